@@ -89,6 +89,11 @@ def lib():
         L.oracle_decode_unit.argtypes = [_i, _i, _i, _i, _i, _i, _i, _i, _i, _i,
                                          _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]
         L.oracle_decode_unit.restype = _i
+        L.oracle_build_unit.argtypes = [_i, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p]
+        L.oracle_build_unit.restype = _i
+        L.oracle_decode_indexed.argtypes = [_i, _i, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p,
+                                            _p, _p, _p, _p, _p, _p, _p]
+        L.oracle_decode_indexed.restype = _i
         L.oracle_merge_partials.argtypes = [_i, _i, _p, _p]
         L.oracle_merge_partials.restype = _i
         _lib = L
@@ -284,6 +289,40 @@ def decode_unit(k, v, q, W, K: int, L: int, center: int = 1, mips: int = 1,
                                   _ptr(c), C.byref(r2), _ptr(logu))
     return {"out": out, "partial": partial, "s_count": s_count, "counts": counts, "in_s": in_s,
             "codes": codes, "qcodes": qcodes, "c": c, "r2": r2.value, "logu": logu, "status": st}
+
+
+def build_unit(k, W, K: int, L: int, center: int = 1, mips: int = 1, sink: int = 4, local: int = 64):
+    """Build half of Alg. 1 for one unit: dict(xbar, n2, codes, c, r2, status)."""
+    k = _c(k, np.uint16)
+    W = _c(W, np.float32)
+    n, d = k.shape
+    dp = d + (1 if mips else 0)
+    xbar = np.zeros((n, dp), np.uint16)
+    n2 = np.zeros(n, np.float64)
+    codes = np.zeros((n, L), np.uint16)
+    c = np.zeros(d, np.float32)
+    r2 = C.c_double(0.0)
+    st = lib().oracle_build_unit(n, d, K, L, center, mips, sink, local, _ptr(k), _ptr(W), _ptr(xbar), _ptr(n2),
+                                 _ptr(codes), _ptr(c), C.byref(r2))
+    return {"xbar": xbar, "n2": n2, "codes": codes, "c": c, "r2": r2.value, "status": st, "K": K, "L": L,
+            "mips": mips, "sink": sink, "local": local, "W": W}
+
+
+def decode_indexed(index, k, v, q, min_collisions: int = 2):
+    """Decode half of Alg. 1 for one unit given oracle.build_unit(...) output."""
+    k, v = _c(k, np.uint16), _c(v, np.uint16)
+    q = _c(q, np.uint16)
+    if q.ndim == 1:
+        q = q[None, :]
+    n, d = k.shape
+    G = q.shape[0]
+    out = np.zeros((G, d), np.float64)
+    s_count = np.zeros(G, np.int32)
+    st = lib().oracle_decode_indexed(n, d, G, index["K"], index["L"], index["mips"], min_collisions,
+                                     index["sink"], index["local"], _ptr(k), _ptr(v), _ptr(q), _ptr(index["W"]),
+                                     _ptr(index["xbar"]), _ptr(index["n2"]), _ptr(index["codes"]), _ptr(out),
+                                     None, _ptr(s_count), None, None, None, None)
+    return {"out": out, "s_count": s_count, "status": st}
 
 
 def decode_batch(k, v, q, W, K, L, center=1, mips=1, min_collisions=2, sink=4, local=64,

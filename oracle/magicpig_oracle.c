@@ -531,25 +531,34 @@ int oracle_estimate(int n, int d, const uint16_t *q, const uint16_t *k, const ui
  *   codes [n][L]; qcodes [G][L]; c [d]; r2; logu [G][n] (only where in S).
  * Returns OR_OK, OR_EINEXACT (contract violated), OR_ENOTREPR,
  * OR_EDEGENERATE (some head with S and T both empty; its out row is 0).    */
-int oracle_decode_unit(int n, int d, int G, int K, int L, int center, int mips,
-                       int min_collisions, int sink, int local, const uint16_t *k,
-                       const uint16_t *v, const uint16_t *q, const float *W, double *out,
-                       double *partial, int32_t *s_count, int32_t *counts_out,
-                       uint8_t *in_s_out, uint16_t *codes_out, uint16_t *qcodes_out,
-                       float *c_out, double *r2_out, double *logu_out) {
-    if (n < 0 || d <= 0 || G <= 0 || K < 1 || K > 16 || L < 1) return OR_EINVAL;
-    if (min_collisions < 1 || min_collisions > L) return OR_EINVAL;
+/* Build half of Algorithm 1 (the hash tables HT): pre-processing
+ * then Encode of every key.  Outputs xbar
+ * [n][d+mips], n2 [n], codes [n][L], c [d], r2.  Returns the transform status. */
+int oracle_build_unit(int n, int d, int K, int L, int center, int mips, int sink, int local,
+                      const uint16_t *k, const float *W, uint16_t *xbar, double *n2,
+                      uint16_t *codes, float *c, double *r2) {
+    if (n < 0 || d <= 0 || K < 1 || K > 16 || L < 1) return OR_EINVAL;
     int dp = d + (mips ? 1 : 0);
     int rc = oracle_check_w(W, (int64_t)dp * K * L);
     if (rc) return rc;
-    float *c = (float *)malloc(sizeof(float) * (size_t)d);
-    uint16_t *xbar = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n > 0 ? n : 1) * dp);
-    double *n2 = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
-    double r2 = 0.0;
-    int status = oracle_key_transform(n, d, k, sink, local, center, mips, c, xbar, n2, &r2,
+    int status = oracle_key_transform(n, d, k, sink, local, center, mips, c, xbar, n2, r2,
                                       NULL, NULL, NULL);
-    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n > 0 ? n : 1) * L);
     oracle_encode_keys(n, dp, xbar, W, K, L, codes);
+    return status;
+}
+
+/* Decode half of Algorithm 1 given the unit's index (xbar, n2,
+ * codes from oracle_build_unit) for G query heads.  Outputs as in
+ * oracle_decode_unit below.  Returns OR_OK or OR_EDEGENERATE. */
+int oracle_decode_indexed(int n, int d, int G, int K, int L, int mips, int min_collisions,
+                          int sink, int local, const uint16_t *k, const uint16_t *v,
+                          const uint16_t *q, const float *W, const uint16_t *xbar,
+                          const double *n2, const uint16_t *codes, double *out, double *partial,
+                          int32_t *s_count, int32_t *counts_out, uint8_t *in_s_out,
+                          uint16_t *qcodes_out, double *logu_out) {
+    if (n < 0 || d <= 0 || G <= 0 || K < 1 || K > 16 || L < 1) return OR_EINVAL;
+    if (min_collisions < 1 || min_collisions > L) return OR_EINVAL;
+    int dp = d + (mips ? 1 : 0);
     uint16_t *qc = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)L);
     int32_t *cnt = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     uint8_t *sel = (uint8_t *)malloc((size_t)(n > 0 ? n : 1));
@@ -602,13 +611,39 @@ int oracle_decode_unit(int n, int d, int G, int K, int L, int center, int mips,
         if (qcodes_out) memcpy(qcodes_out + (size_t)g * L, qc, sizeof(uint16_t) * (size_t)L);
         if (logu_out) memcpy(logu_out + (size_t)g * n, logu, sizeof(double) * (size_t)n);
     }
+    free(qc); free(cnt); free(sel); free(logu); free(o); free(a);
+    return degenerate ? OR_EDEGENERATE : OR_OK;
+}
+
+/* Algorithm 1 end to end for one unit: oracle_build_unit + oracle_decode_indexed. */
+int oracle_decode_unit(int n, int d, int G, int K, int L, int center, int mips,
+                       int min_collisions, int sink, int local, const uint16_t *k,
+                       const uint16_t *v, const uint16_t *q, const float *W, double *out,
+                       double *partial, int32_t *s_count, int32_t *counts_out,
+                       uint8_t *in_s_out, uint16_t *codes_out, uint16_t *qcodes_out,
+                       float *c_out, double *r2_out, double *logu_out) {
+    if (n < 0 || d <= 0 || G <= 0 || K < 1 || K > 16 || L < 1) return OR_EINVAL;
+    if (min_collisions < 1 || min_collisions > L) return OR_EINVAL;
+    int dp = d + (mips ? 1 : 0);
+    float *c = (float *)malloc(sizeof(float) * (size_t)d);
+    uint16_t *xbar = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n > 0 ? n : 1) * dp);
+    double *n2 = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n > 0 ? n : 1) * L);
+    double r2 = 0.0;
+    int status = oracle_build_unit(n, d, K, L, center, mips, sink, local, k, W, xbar, n2, codes, c, &r2);
+    if (status == OR_ENOTREPR || status == OR_EINVAL) {
+        free(c); free(xbar); free(n2); free(codes);
+        return status;
+    }
+    int rc = oracle_decode_indexed(n, d, G, K, L, mips, min_collisions, sink, local, k, v, q, W,
+                                   xbar, n2, codes, out, partial, s_count, counts_out, in_s_out,
+                                   qcodes_out, logu_out);
     if (codes_out) memcpy(codes_out, codes, sizeof(uint16_t) * (size_t)n * L);
     if (c_out) memcpy(c_out, c, sizeof(float) * (size_t)d);
     if (r2_out) *r2_out = r2;
-    free(c); free(xbar); free(n2); free(codes); free(qc); free(cnt); free(sel);
-    free(logu); free(o); free(a);
+    free(c); free(xbar); free(n2); free(codes);
     if (status) return status;
-    return degenerate ? OR_EDEGENERATE : OR_OK;
+    return rc;
 }
 
 /* Merge of partial softmax states ("recursive attention"):

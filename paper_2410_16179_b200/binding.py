@@ -1,0 +1,245 @@
+"""Thin ctypes binding of libmagicpig.so (include/magicpig.h).
+
+Argument marshalling only: every step of the method runs in the CUDA kernels
+behind the C ABI.  Tensors are torch CUDA tensors (bf16 data as
+torch.bfloat16); they are passed as raw device pointers on the current torch
+stream.  There is no CPU fallback: if the shared library or a GPU is missing,
+loading raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import torch
+
+from . import build as _build
+
+_p = C.c_void_p
+_i = C.c_int
+_i64 = C.c_int64
+_sz = C.c_size_t
+
+OK, EINVAL, ENOTREPR, EDEGENERATE, ECUDA, EWORKSPACE, EINEXACT, EOVERFLOW = 0, -1, -2, -3, -4, -5, -6, -7
+STATUS_INEXACT, STATUS_OVERFLOW, STATUS_DEGENERATE, STATUS_NOTREPR = 1, 2, 4, 8
+PART = 130
+HEAD_DIM = 128
+
+
+class magicpig_config(C.Structure):
+    _fields_ = [("K", C.c_int32), ("L", C.c_int32), ("head_dim", C.c_int32), ("center", C.c_int32),
+                ("mips", C.c_int32), ("min_collisions", C.c_int32), ("sink", C.c_int32), ("local", C.c_int32)]
+
+
+def make_config(K=10, L=150, center=1, mips=1, min_collisions=2, sink=4, local=64) -> magicpig_config:
+    return magicpig_config(K, L, HEAD_DIM, center, mips, min_collisions, sink, local)
+
+
+_SIGS = {
+    "magicpig_validate_config": ([_p], _i),
+    "magicpig_codes_words": ([_p, _i64, _i64, _i64], _sz),
+    "magicpig_build_workspace_bytes": ([_p, _i64, _i64, _i64], _sz),
+    "magicpig_decode_workspace_bytes": ([_p, _i64, _i64, _i64, _i64], _sz),
+    "magicpig_workspace_init": ([_p, _sz, _p], _i),
+    "magicpig_workspace_status": ([_p, _p, _p], _i),
+    "magicpig_key_stats": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _sz, _p], _i),
+    "magicpig_key_norms": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_reduce_stats": ([_i, _p, _p, _i, _i64, _i64, _p, _p, _p], _i),
+    "magicpig_build_tables": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_build_index": ([_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_decode": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p,
+                         _p, _sz, _p], _i),
+    "magicpig_encode_queries": ([_p, _p, _i64, _i64, _p, _p, _sz, _p], _i),
+    "magicpig_decode_encoded": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p,
+                                 _p, _sz, _p], _i),
+    "magicpig_merge_partials": ([_p, _i, _i64, _p, _p], _i),
+    "magicpig_export_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
+    "magicpig_import_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
+    "magicpig_query_codes": ([_p, _p, _i64, _i64, _p, _p, _p, _sz, _p], _i),
+    "magicpig_collision_counts": ([_p, _p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _sz, _p], _i),
+    "magicpig_debug_hash_acc": ([_p, _p, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_strerror": ([_i], C.c_char_p),
+    "magicpig_version": ([], C.c_char_p),
+    "magicpig_launch_count": ([], C.c_uint64),
+}
+
+_lib = None
+
+
+def lib(load_only: bool = False):
+    """Load the in-tree shared library (building it if stale)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path) or not load_only:
+            path = _build.build()
+        L = C.CDLL(path)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+class MagicPIGError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str):
+    if rc != OK:
+        raise MagicPIGError(f"{what}: {lib().magicpig_strerror(rc).decode()} ({rc})")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise MagicPIGError("expected a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise MagicPIGError("expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _cfg(cfg):
+    return C.byref(cfg)
+
+
+# ---------------------------------------------------------------- sizes
+def codes_words(cfg, B, Hkv, n):
+    return int(lib().magicpig_codes_words(_cfg(cfg), B, Hkv, n))
+
+
+def build_workspace_bytes(cfg, B, Hkv, n):
+    return int(lib().magicpig_build_workspace_bytes(_cfg(cfg), B, Hkv, n))
+
+
+def decode_workspace_bytes(cfg, B, Hq, Hkv, n):
+    return int(lib().magicpig_decode_workspace_bytes(_cfg(cfg), B, Hq, Hkv, n))
+
+
+def new_workspace(nbytes: int, device="cuda") -> torch.Tensor:
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    workspace_init(ws)
+    return ws
+
+
+def workspace_init(ws):
+    _check(lib().magicpig_workspace_init(_ptr(ws), ws.numel(), _stream()), "workspace_init")
+
+
+def workspace_status(ws) -> int:
+    st = C.c_uint32(0)
+    _check(lib().magicpig_workspace_status(_ptr(ws), C.byref(st), _stream()), "workspace_status")
+    return int(st.value)
+
+
+# ---------------------------------------------------------------- build
+def key_stats(cfg, k, seq_offset, n_global, key_sum, count, ws):
+    B, Hkv, n, _ = k.shape
+    _check(lib().magicpig_key_stats(_cfg(cfg), _ptr(k), B, Hkv, n, seq_offset, n_global, _ptr(key_sum),
+                                    _ptr(count), _ptr(ws), ws.numel(), _stream()), "key_stats")
+
+
+def key_norms(cfg, k, seq_offset, n_global, key_sum, count, center, r2, ws):
+    B, Hkv, n, _ = k.shape
+    _check(lib().magicpig_key_norms(_cfg(cfg), _ptr(k), B, Hkv, n, seq_offset, n_global, _ptr(key_sum),
+                                    _ptr(count), _ptr(center), _ptr(r2), _ptr(ws), ws.numel(), _stream()),
+           "key_norms")
+
+
+def reduce_stats(mode, parts_sum, parts_cnt, P, B, Hkv, out_sum, out_cnt):
+    _check(lib().magicpig_reduce_stats(mode, _ptr(parts_sum), _ptr(parts_cnt), P, B, Hkv, _ptr(out_sum),
+                                       _ptr(out_cnt), _stream()), "reduce_stats")
+
+
+def build_tables(cfg, k, seq_offset, n_global, W, center, r2, codes, ws):
+    B, Hkv, n, _ = k.shape
+    _check(lib().magicpig_build_tables(_cfg(cfg), _ptr(k), B, Hkv, n, seq_offset, n_global, _ptr(W),
+                                       _ptr(center), _ptr(r2), _ptr(codes), _ptr(ws), ws.numel(), _stream()),
+           "build_tables")
+
+
+def build_index(cfg, k, W, center, r2, codes, key_sum, count, ws):
+    B, Hkv, n, _ = k.shape
+    _check(lib().magicpig_build_index(_cfg(cfg), _ptr(k), B, Hkv, n, _ptr(W), _ptr(center), _ptr(r2),
+                                      _ptr(codes), _ptr(key_sum), _ptr(count), _ptr(ws), ws.numel(), _stream()),
+           "build_index")
+
+
+# ---------------------------------------------------------------- decode
+def decode(cfg, q, codes, center, r2, k, v, seq_offset, n_global, W, ws, out=None, partial=None,
+           s_count=None, s_mask=None):
+    B, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    _check(lib().magicpig_decode(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(r2), _ptr(k), _ptr(v),
+                                 B, Hkv, n, seq_offset, n_global, _ptr(W), _ptr(out), _ptr(partial),
+                                 _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(), _stream()), "decode")
+
+
+def encode_queries(cfg, q, W, ws):
+    Bn, Hq, _ = q.shape
+    _check(lib().magicpig_encode_queries(_cfg(cfg), _ptr(q), Bn, Hq, _ptr(W), _ptr(ws), ws.numel(), _stream()),
+           "encode_queries")
+
+
+def decode_encoded(cfg, q, codes, center, r2, k, v, seq_offset, n_global, ws, out=None, partial=None,
+                   s_count=None, s_mask=None):
+    Bn, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    _check(lib().magicpig_decode_encoded(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(r2), _ptr(k),
+                                         _ptr(v), Bn, Hkv, n, seq_offset, n_global, _ptr(out), _ptr(partial),
+                                         _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(), _stream()),
+           "decode_encoded")
+
+
+def merge_partials(parts, out):
+    P, BH, _ = parts.shape
+    _check(lib().magicpig_merge_partials(_ptr(parts), P, BH, _ptr(out), _stream()), "merge_partials")
+
+
+# ---------------------------------------------------------------- debug
+def export_codes(cfg, codes, B, Hkv, n, canonical):
+    _check(lib().magicpig_export_codes(_cfg(cfg), _ptr(codes), B, Hkv, n, _ptr(canonical), _stream()),
+           "export_codes")
+
+
+def import_codes(cfg, canonical, B, Hkv, n, codes):
+    _check(lib().magicpig_import_codes(_cfg(cfg), _ptr(canonical), B, Hkv, n, _ptr(codes), _stream()),
+           "import_codes")
+
+
+def query_codes(cfg, q, W, qcodes, ws):
+    B, Hq, _ = q.shape
+    _check(lib().magicpig_query_codes(_cfg(cfg), _ptr(q), B, Hq, _ptr(W), _ptr(qcodes), _ptr(ws), ws.numel(),
+                                      _stream()), "query_codes")
+
+
+def collision_counts(cfg, q, codes, k_shape, W, counts, ws):
+    B, Hkv, n = k_shape[:3]
+    Hq = q.shape[1]
+    _check(lib().magicpig_collision_counts(_cfg(cfg), _ptr(q), Hq, _ptr(codes), B, Hkv, n, _ptr(W), _ptr(counts),
+                                           _ptr(ws), ws.numel(), _stream()), "collision_counts")
+
+
+def debug_hash_acc(cfg, k_unit, W, center, r2, acc, ws):
+    n = k_unit.shape[0]
+    _check(lib().magicpig_debug_hash_acc(_cfg(cfg), _ptr(k_unit), n, _ptr(W), _ptr(center), _ptr(r2), _ptr(acc),
+                                         _ptr(ws), ws.numel(), _stream()), "debug_hash_acc")
+
+
+def launch_count() -> int:
+    return int(lib().magicpig_launch_count())
+
+
+def version() -> str:
+    return lib().magicpig_version().decode()

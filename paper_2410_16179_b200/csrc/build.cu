@@ -1,0 +1,327 @@
+// build.cu -- key statistics, centering, MIPS transform and operand
+// preparation for the hash GEMM (PAPER.md:124-127 centering, P:49-55 MIPS).
+//
+// All bandwidth-bound (one pass over K per phase): 128-bit loads of key rows,
+// exact integer (fixed-point 2^-64) accumulation so that every reduction is
+// order-independent and bit-reproducible (reading R2b).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mp {
+
+constexpr float ABS_LIMIT = 134217728.0f;  // 2^27
+
+// is global position `pos` static (sink / local window)? (R12)
+__device__ __forceinline__ bool is_static_pos(int64_t pos, int64_t n_global, int sink, int local) {
+    return pos < (int64_t)sink || pos >= n_global - (int64_t)local;
+}
+
+// ---------------------------------------------------------------------------
+// Phase 1: per (unit, split, dim) partial sums of q64(k) over dynamic keys.
+// grid (nsplit, units), block 128 (thread = dim).
+__global__ void __launch_bounds__(128) key_stats_partial_kernel(
+    const uint16_t* __restrict__ k, int64_t n_local, int64_t seq_offset, int64_t n_global, int sink,
+    int local, int64_t* __restrict__ part_sum, int64_t* __restrict__ part_cnt, uint32_t* status) {
+    const int d = threadIdx.x;
+    const int64_t unit = blockIdx.y;
+    const int split = blockIdx.x, nsplit = gridDim.x;
+    const int64_t i0 = (int64_t)split * STATS_SPLIT;
+    const int64_t i1 = min(i0 + (int64_t)STATS_SPLIT, n_local);
+    const uint16_t* kp = k + unit * n_local * HD;
+    i128 acc = 0;
+    int cnt = 0;
+    bool bad = false;
+    for (int64_t i = i0; i < i1; i++) {
+        if (is_static_pos(seq_offset + i, n_global, sink, local)) continue;
+        uint16_t h = kp[i * HD + d];
+        bad |= fabsf(bf2f(h)) >= ABS_LIMIT;
+        acc += q64_of_bf16(h);
+        cnt++;
+    }
+    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
+    st_q64(part_sum + ((unit * nsplit + split) * HD + d) * 2, acc);
+    if (d == 0) part_cnt[unit * nsplit + split] = cnt;
+}
+
+// Sum of P partial copies: out[u][d] = sum_p part[u][p][d]  (fixed order)
+// grid (units), block 128
+__global__ void __launch_bounds__(128) sum_parts_kernel(const int64_t* __restrict__ part_sum,
+                                                        const int64_t* __restrict__ part_cnt, int nsplit,
+                                                        int64_t* __restrict__ key_sum,
+                                                        int64_t* __restrict__ count) {
+    const int d = threadIdx.x;
+    const int64_t unit = blockIdx.x;
+    i128 acc = 0;
+    int64_t c = 0;
+    for (int p = 0; p < nsplit; p++) {
+        acc += ld_q64(part_sum + ((unit * nsplit + p) * HD + d) * 2);
+        c += part_cnt[unit * nsplit + p];
+    }
+    st_q64(key_sum + (unit * HD + d) * 2, acc);
+    if (d == 0) count[unit] = c;
+}
+
+// Shard reduction (after an all-gather): mode 0 sum of key sums and counts,
+// mode 1 max of r2.  grid (ceil(units*128/256)), block 256.
+__global__ void reduce_shards_kernel(int mode, const int64_t* __restrict__ parts_sum,
+                                     const int64_t* __restrict__ parts_cnt, int P, int64_t units,
+                                     int64_t* __restrict__ out_sum, int64_t* __restrict__ out_cnt) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (mode == 0) {
+        int64_t nel = units * HD;
+        if (idx < nel) {
+            i128 acc = 0;
+            for (int p = 0; p < P; p++) acc += ld_q64(parts_sum + ((int64_t)p * nel + idx) * 2);
+            st_q64(out_sum + idx * 2, acc);
+        }
+        if (idx < units) {
+            int64_t c = 0;
+            for (int p = 0; p < P; p++) c += parts_cnt[(int64_t)p * units + idx];
+            out_cnt[idx] = c;
+        }
+    } else {
+        if (idx < units) {
+            i128 m = 0;
+            for (int p = 0; p < P; p++) {
+                i128 v = ld_q64(parts_sum + ((int64_t)p * units + idx) * 2);
+                m = v > m ? v : m;
+            }
+            st_q64(out_sum + idx * 2, m);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 2a: centering vector c = fl32(fl64(fl64(sum 2^-64) / count)).
+// grid (units), block 128
+__global__ void __launch_bounds__(128) center_kernel(const int64_t* __restrict__ key_sum,
+                                                     const int64_t* __restrict__ count, int do_center,
+                                                     float* __restrict__ center) {
+    const int d = threadIdx.x;
+    const int64_t unit = blockIdx.x;
+    float c = 0.0f;
+    int64_t n = count[unit];
+    if (do_center && n > 0) {
+        double s = q64_to_double(ld_q64(key_sum + (unit * HD + d) * 2));
+        c = (float)(s / (double)n);
+    }
+    center[unit * HD + d] = c;
+}
+
+// x = bf16(fl32(k - c)) for the 4 dims of this lane; returns q64 sum of x^2
+__device__ __forceinline__ u128 transform4(uint2 kraw, float4 c, uint32_t& x01, uint32_t& x23,
+                                           bool& bad) {
+    float k0 = __uint_as_float(kraw.x << 16), k1 = __uint_as_float(kraw.x & 0xFFFF0000u);
+    float k2 = __uint_as_float(kraw.y << 16), k3 = __uint_as_float(kraw.y & 0xFFFF0000u);
+    uint16_t b0 = f2bf_rn(__fsub_rn(k0, c.x)), b1 = f2bf_rn(__fsub_rn(k1, c.y));
+    uint16_t b2 = f2bf_rn(__fsub_rn(k2, c.z)), b3 = f2bf_rn(__fsub_rn(k3, c.w));
+    float f0 = bf2f(b0), f1 = bf2f(b1), f2 = bf2f(b2), f3 = bf2f(b3);
+    bad |= fabsf(f0) >= ABS_LIMIT || fabsf(f1) >= ABS_LIMIT || fabsf(f2) >= ABS_LIMIT ||
+           fabsf(f3) >= ABS_LIMIT;
+    x01 = (uint32_t)b0 | ((uint32_t)b1 << 16);
+    x23 = (uint32_t)b2 | ((uint32_t)b3 << 16);
+    // squares of bf16 values are exact in fp32 (16 significant bits)
+    return q64_of_f32(__fmul_rn(f0, f0)) + q64_of_f32(__fmul_rn(f1, f1)) + q64_of_f32(__fmul_rn(f2, f2)) +
+           q64_of_f32(__fmul_rn(f3, f3));
+}
+
+__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v += shfl_xor_u128(v, m);
+    return v;
+}
+
+// Phase 2b: per (unit, split) partial max of n2q over dynamic keys.
+// grid (nsplit, units), block 256 (8 warps; warp per key, lane = 4 dims)
+__global__ void __launch_bounds__(256) r2_partial_kernel(const uint16_t* __restrict__ k, int64_t n_local,
+                                                         int64_t seq_offset, int64_t n_global, int sink,
+                                                         int local, const float* __restrict__ center,
+                                                         int64_t* __restrict__ part_r2, uint32_t* status) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t unit = blockIdx.y;
+    const int split = blockIdx.x, nsplit = gridDim.x;
+    const int64_t i0 = (int64_t)split * STATS_SPLIT;
+    const int64_t i1 = min(i0 + (int64_t)STATS_SPLIT, n_local);
+    const float4 c = reinterpret_cast<const float4*>(center + unit * HD)[lane];
+    const uint16_t* kp = k + unit * n_local * HD;
+    u128 best = 0;
+    bool bad = false;
+    for (int64_t i = i0 + warp; i < i1; i += 8) {
+        if (is_static_pos(seq_offset + i, n_global, sink, local)) continue;
+        uint2 kr = reinterpret_cast<const uint2*>(kp + i * HD)[lane];
+        uint32_t a, b;
+        u128 s = warp_sum_u128(transform4(kr, c, a, b, bad));
+        best = s > best ? s : best;
+    }
+    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
+    __shared__ unsigned long long sm[8][2];
+    if (lane == 0) {
+        sm[warp][0] = (unsigned long long)best;
+        sm[warp][1] = (unsigned long long)(best >> 64);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 m = 0;
+        for (int w = 0; w < 8; w++) {
+            u128 v = ((u128)sm[w][1] << 64) | (u128)sm[w][0];
+            m = v > m ? v : m;
+        }
+        st_q64(part_r2 + (unit * nsplit + split) * 2, (i128)m);
+    }
+}
+
+// max over splits -> r2[unit]; grid (ceil(units/128)), block 128
+__global__ void max_parts_kernel(const int64_t* __restrict__ part_r2, int nsplit, int64_t units,
+                                 int64_t* __restrict__ r2) {
+    int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= units) return;
+    i128 m = 0;
+    for (int p = 0; p < nsplit; p++) {
+        i128 v = ld_q64(part_r2 + (u * nsplit + p) * 2);
+        m = v > m ? v : m;
+    }
+    st_q64(r2 + u * 2, m);
+}
+
+// ---------------------------------------------------------------------------
+// Phase 3a: hashed key vectors xbar_i = [bf16(fl32(k - c)), s_i, 0...] written
+// straight into the UMMA canonical K-major no-swizzle layout, one 128-row tile
+// per 128*KD*2 bytes: element (r, kk) at ((kk/8)*16 + r/8)*128 + (r%8)*16 + (kk%8)*2.
+// Also |xbar_i| (fp32, for the filter threshold; -1 for padding rows).
+// grid (ceil(n_pad/8), units), block 256 (warp per key)
+__global__ void __launch_bounds__(256) prep_x_kernel(const uint16_t* __restrict__ k, int64_t n_local,
+                                                     int64_t n_pad, int mips, int KD,
+                                                     const float* __restrict__ center,
+                                                     const int64_t* __restrict__ r2,
+                                                     uint8_t* __restrict__ xt, float* __restrict__ xnorm,
+                                                     uint32_t* status) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t unit = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * 8 + warp;
+    if (i >= n_pad) return;
+    const int64_t tile = i >> 7;
+    const int r = (int)(i & 127);
+    uint8_t* tbase = xt + (unit * (n_pad >> 7) + tile) * (int64_t)(128 * KD * 2);
+    const int rowoff = (r >> 3) * 128 + (r & 7) * 16;
+    uint32_t a = 0, b = 0;
+    u128 n2 = 0;
+    bool bad = false;
+    if (i < n_local) {
+        const float4 c = reinterpret_cast<const float4*>(center + unit * HD)[lane];
+        uint2 kr = reinterpret_cast<const uint2*>(k + (unit * n_local + i) * HD)[lane];
+        n2 = warp_sum_u128(transform4(kr, c, a, b, bad));
+    }
+    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
+    // dims kk = 4*lane .. 4*lane+3: chunk kk/8 = lane/2, offset (lane&1)*8 bytes
+    *reinterpret_cast<uint2*>(tbase + (lane >> 1) * 16 * 128 + rowoff + (lane & 1) * 8) = make_uint2(a, b);
+    if (lane < (KD - HD) / 8) {
+        uint16_t s = 0;
+        double n2d = q64_to_double((i128)n2);
+        if (mips && lane == 0 && i < n_local) {
+            i128 rr = ld_q64(r2 + unit * 2);
+            i128 diff = rr - (i128)n2;
+            s = diff > 0 ? d2bf_rn_pos(sqrt(q64_to_double(diff))) : (uint16_t)0;
+        }
+        uint4 v = make_uint4((uint32_t)s, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(tbase + (16 + lane) * 16 * 128 + rowoff) = v;
+        if (lane == 0) {
+            float sf = bf2f(s);
+            xnorm[unit * n_pad + i] = i < n_local ? (float)sqrt(n2d + (double)sf * (double)sf) : -1.0f;
+        }
+    } else if (KD == HD && lane == 0) {
+        xnorm[unit * n_pad + i] = i < n_local ? (float)sqrt(q64_to_double((i128)n2)) : -1.0f;
+    }
+}
+
+// Phase 3b: projections W [dp][KL] fp32 -> bf16 tiles of 64 columns in the
+// same canonical layout (element (c, kk) at ((kk/8)*8 + c/8)*128 + (c%8)*16 +
+// (kk%8)*2), zero padded to KD rows and NT*64 columns; wmax = max_j |W_j|.
+// grid (NT), block 64 (thread = column)
+__global__ void __launch_bounds__(64) prep_w_kernel(const float* __restrict__ W, int dp, int KL, int KD,
+                                                    uint8_t* __restrict__ wt, float* __restrict__ wmax,
+                                                    uint32_t* status) {
+    const int c = threadIdx.x;
+    const int j = blockIdx.x * 64 + c;
+    uint8_t* tbase = wt + (int64_t)blockIdx.x * (64 * KD * 2);
+    const int rowoff = (c >> 3) * 128 + (c & 7) * 16;
+    float nrm = 0.0f;
+    bool notrepr = false;
+    for (int kc = 0; kc < KD / 8; kc++) {
+        uint32_t h[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            uint32_t lo = 0, hi = 0;
+            int kk = kc * 8 + 2 * t;
+            if (j < KL && kk < dp) {
+                uint32_t u = __float_as_uint(W[(int64_t)kk * KL + j]);
+                notrepr |= (u & 0xFFFFu) != 0;
+                lo = u >> 16;
+                float f = bf2f((uint16_t)lo);
+                nrm = fmaf(f, f, nrm);
+            }
+            if (j < KL && kk + 1 < dp) {
+                uint32_t u = __float_as_uint(W[(int64_t)(kk + 1) * KL + j]);
+                notrepr |= (u & 0xFFFFu) != 0;
+                hi = u >> 16;
+                float f = bf2f((uint16_t)hi);
+                nrm = fmaf(f, f, nrm);
+            }
+            h[t] = lo | (hi << 16);
+        }
+        *reinterpret_cast<uint4*>(tbase + kc * 8 * 128 + rowoff) = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+    if (notrepr) atomicOr(status, MAGICPIG_STATUS_NOTREPR);
+    // positive floats order like their bit patterns
+    float nr = sqrtf(nrm) * (1.0f + 0x1p-10f);
+    atomicMax(reinterpret_cast<unsigned int*>(wmax), __float_as_uint(nr));
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+int launch_key_stats(const uint16_t* k, int64_t units, int64_t n_local, int64_t seq_offset,
+                     int64_t n_global, int sink, int local, int64_t* part_sum, int64_t* part_cnt,
+                     int64_t* key_sum, int64_t* count, uint32_t* status, cudaStream_t st) {
+    int nsplit = (int)((n_local + STATS_SPLIT - 1) / STATS_SPLIT);
+    if (nsplit < 1) nsplit = 1;
+    key_stats_partial_kernel<<<dim3(nsplit, (unsigned)units), 128, 0, st>>>(
+        k, n_local, seq_offset, n_global, sink, local, part_sum, part_cnt, status);
+    sum_parts_kernel<<<(unsigned)units, 128, 0, st>>>(part_sum, part_cnt, nsplit, key_sum, count);
+    count_launch(2);
+    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_key_norms(const uint16_t* k, int64_t units, int64_t n_local, int64_t seq_offset,
+                     int64_t n_global, int sink, int local, int do_center, const int64_t* key_sum,
+                     const int64_t* count, float* center, int64_t* part_r2, int64_t* r2, uint32_t* status,
+                     cudaStream_t st) {
+    int nsplit = (int)((n_local + STATS_SPLIT - 1) / STATS_SPLIT);
+    if (nsplit < 1) nsplit = 1;
+    center_kernel<<<(unsigned)units, 128, 0, st>>>(key_sum, count, do_center, center);
+    r2_partial_kernel<<<dim3(nsplit, (unsigned)units), 256, 0, st>>>(k, n_local, seq_offset, n_global, sink,
+                                                                     local, center, part_r2, status);
+    max_parts_kernel<<<(unsigned)((units + 127) / 128), 128, 0, st>>>(part_r2, nsplit, units, r2);
+    count_launch(3);
+    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_reduce_shards(int mode, const int64_t* parts_sum, const int64_t* parts_cnt, int P, int64_t units,
+                         int64_t* out_sum, int64_t* out_cnt, cudaStream_t st) {
+    int64_t n = mode == 0 ? units * HD : units;
+    reduce_shards_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(mode, parts_sum, parts_cnt, P, units,
+                                                                      out_sum, out_cnt);
+    count_launch(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad, int mips, int KD,
+                const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, const float* W, int KL,
+                int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st) {
+    cudaMemsetAsync(wmax, 0, sizeof(float), st);
+    prep_x_kernel<<<dim3((unsigned)((n_pad + 7) / 8), (unsigned)units), 256, 0, st>>>(
+        k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, status);
+    prep_w_kernel<<<NT, 64, 0, st>>>(W, HD + (mips ? 1 : 0), KL, KD, wt, wmax, status);
+    count_launch(2);
+    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+}  // namespace mp

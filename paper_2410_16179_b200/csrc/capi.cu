@@ -1,0 +1,411 @@
+// capi.cu -- the C ABI (include/magicpig.h): validation, workspace layout,
+// launch sequencing.  No allocation, no global state besides a launch counter.
+#include <atomic>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mp {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+static bool cfg_ok(const magicpig_config* c) {
+    if (!c) return false;
+    if (c->head_dim != HD) return false;
+    if (c->K < 1 || c->K > 16) return false;
+    if (c->L < 1 || c->L > 1024) return false;
+    if (c->min_collisions < 1 || c->min_collisions > 2 || c->L < c->min_collisions) return false;
+    if (c->center < 0 || c->center > 1 || c->mips < 0 || c->mips > 1) return false;
+    if (c->sink < 0 || c->local < 0) return false;
+    return true;
+}
+
+static bool shape_ok(int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global) {
+    if (B < 1 || Hkv < 1 || n_local < 0 || seq_offset < 0) return false;
+    if (seq_offset + n_local > n_global) return false;
+    if (n_local > ((int64_t)1 << 31) - KCHUNK) return false;
+    return true;
+}
+
+// ---------------------------------------------------------------- layouts
+struct BuildWs {
+    uint32_t* status;
+    float* wmax;
+    uint32_t* fix_count;
+    int64_t* part_sum;
+    int64_t* part_cnt;
+    int64_t* part_r2;
+    uint8_t* xt;
+    float* xnorm;
+    uint8_t* wt;
+    uint2* fix_list;
+    uint32_t fix_cap;
+    int64_t n_pad;
+    int nsplit, KD, NT;
+    size_t bytes;
+};
+
+static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, int64_t n_local, void* base) {
+    BuildWs w;
+    memset(&w, 0, sizeof(w));
+    const Geom g = make_geom(c->K, c->L, n_local);
+    const int64_t units = B * Hkv;
+    w.n_pad = ((n_local + KCHUNK - 1) / KCHUNK) * KCHUNK;
+    w.nsplit = (int)((n_local + STATS_SPLIT - 1) / STATS_SPLIT);
+    if (w.nsplit < 1) w.nsplit = 1;
+    w.KD = c->mips ? 144 : 128;
+    int cols = g.KL > g.KLq * 4 ? g.KL : g.KLq * 4;
+    w.NT = (cols + 63) / 64;
+    int64_t dots = units * w.n_pad * (int64_t)w.NT * 64;
+    int64_t cap = dots / 512;
+    if (cap < 65536) cap = 65536;
+    if (cap > 0x7fffffffLL) cap = 0x7fffffffLL;
+    w.fix_cap = (uint32_t)cap;
+    uint8_t* p = (uint8_t*)base;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p ? p + off : nullptr;
+        off += align256(bytes);
+        return r;
+    };
+    uint8_t* hdr = take(256);
+    w.status = (uint32_t*)hdr;
+    w.wmax = hdr ? (float*)(hdr + 4) : nullptr;
+    w.fix_count = hdr ? (uint32_t*)(hdr + 8) : nullptr;
+    w.part_sum = (int64_t*)take((size_t)units * w.nsplit * HD * 16);
+    w.part_cnt = (int64_t*)take((size_t)units * w.nsplit * 8);
+    w.part_r2 = (int64_t*)take((size_t)units * w.nsplit * 16);
+    w.xt = take((size_t)units * w.n_pad * w.KD * 2);
+    w.xnorm = (float*)take((size_t)units * w.n_pad * 4);
+    w.wt = take((size_t)w.NT * 64 * w.KD * 2);
+    w.fix_list = (uint2*)take((size_t)w.fix_cap * 8);
+    w.bytes = off;
+    return w;
+}
+
+struct DecodeWs {
+    uint32_t* status;
+    uint32_t* qbits;
+    uint32_t* seen;
+    uint32_t* chunk_ctr;
+    uint32_t* unit_ctr;
+    float* parts;
+    int32_t* chunk_cnt;
+    size_t bytes;
+};
+
+static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, int64_t Hkv, int64_t n_local,
+                              void* base) {
+    DecodeWs w;
+    memset(&w, 0, sizeof(w));
+    const Geom g = make_geom(c->K, c->L, n_local);
+    const int64_t units = B * Hkv;
+    const int64_t G = Hq / Hkv;
+    const int64_t nch = g.nchunks > 0 ? g.nchunks : 1;
+    uint8_t* p = (uint8_t*)base;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p ? p + off : nullptr;
+        off += align256(bytes);
+        return r;
+    };
+    w.status = (uint32_t*)take(256);
+    w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
+    w.seen = (uint32_t*)take((size_t)units * nch * G * 64 * 4);
+    w.chunk_ctr = (uint32_t*)take((size_t)units * nch * 4);
+    w.unit_ctr = (uint32_t*)take((size_t)units * 4);
+    w.parts = (float*)take((size_t)units * nch * G * PART * 4);
+    w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
+    w.bytes = off;
+    return w;
+}
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" {
+
+int magicpig_validate_config(const magicpig_config* cfg) { return cfg_ok(cfg) ? MAGICPIG_OK : MAGICPIG_EINVAL; }
+
+size_t magicpig_codes_words(const magicpig_config* cfg, int64_t B, int64_t Hkv, int64_t n_local) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || n_local < 0) return 0;
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    return (size_t)(B * Hkv) * (size_t)g.nchunks * (size_t)g.KLq * 128;
+}
+
+size_t magicpig_build_workspace_bytes(const magicpig_config* cfg, int64_t B, int64_t Hkv, int64_t n_local) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || n_local < 0) return 0;
+    return build_layout(cfg, B, Hkv, n_local, nullptr).bytes;
+}
+
+size_t magicpig_decode_workspace_bytes(const magicpig_config* cfg, int64_t B, int64_t Hq, int64_t Hkv,
+                                       int64_t n_local) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || Hq < Hkv || Hq % Hkv || n_local < 0) return 0;
+    return decode_layout(cfg, B, Hq, Hkv, n_local, nullptr).bytes;
+}
+
+int magicpig_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+    if (!ws) return MAGICPIG_EINVAL;
+    return cudaMemsetAsync(ws, 0, ws_bytes, S(stream)) == cudaSuccess ? MAGICPIG_OK : MAGICPIG_ECUDA;
+}
+
+int magicpig_workspace_status(void* ws, uint32_t* status, void* stream) {
+    if (!ws || !status) return MAGICPIG_EINVAL;
+    if (cudaMemcpyAsync(status, ws, 4, cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess) return MAGICPIG_ECUDA;
+    if (cudaMemsetAsync(ws, 0, 4, S(stream)) != cudaSuccess) return MAGICPIG_ECUDA;
+    return cudaStreamSynchronize(S(stream)) == cudaSuccess ? MAGICPIG_OK : MAGICPIG_ECUDA;
+}
+
+int magicpig_key_stats(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n_local,
+                       int64_t seq_offset, int64_t n_global, int64_t* key_sum, int64_t* count, void* ws,
+                       size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
+    if (!key_sum || !count || !ws || (n_local > 0 && !k)) return MAGICPIG_EINVAL;
+    BuildWs w = build_layout(cfg, B, Hkv, n_local, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    return launch_key_stats(k, B * Hkv, n_local, seq_offset, n_global, cfg->sink, cfg->local, w.part_sum,
+                            w.part_cnt, key_sum, count, w.status, S(stream));
+}
+
+int magicpig_key_norms(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n_local,
+                       int64_t seq_offset, int64_t n_global, const int64_t* key_sum, const int64_t* count,
+                       float* center, int64_t* r2, void* ws, size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
+    if (!key_sum || !count || !center || !r2 || !ws || (n_local > 0 && !k)) return MAGICPIG_EINVAL;
+    BuildWs w = build_layout(cfg, B, Hkv, n_local, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    return launch_key_norms(k, B * Hkv, n_local, seq_offset, n_global, cfg->sink, cfg->local, cfg->center, key_sum,
+                            count, center, w.part_r2, r2, w.status, S(stream));
+}
+
+int magicpig_reduce_stats(int mode, const int64_t* parts_sum, const int64_t* parts_cnt, int P, int64_t B,
+                          int64_t Hkv, int64_t* out_sum, int64_t* out_cnt, void* stream) {
+    if ((mode != 0 && mode != 1) || P < 1 || B < 1 || Hkv < 1 || !parts_sum || !out_sum) return MAGICPIG_EINVAL;
+    if (mode == 0 && (!parts_cnt || !out_cnt)) return MAGICPIG_EINVAL;
+    return launch_reduce_shards(mode, parts_sum, parts_cnt, P, B * Hkv, out_sum, out_cnt, S(stream));
+}
+
+int magicpig_build_tables(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n_local,
+                          int64_t seq_offset, int64_t n_global, const float* W, const float* center,
+                          const int64_t* r2, uint32_t* codes, void* ws, size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
+    if (!W || !center || !r2 || !codes || !ws || (n_local > 0 && !k)) return MAGICPIG_EINVAL;
+    BuildWs w = build_layout(cfg, B, Hkv, n_local, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    if (n_local == 0) return MAGICPIG_OK;
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    cudaStream_t st = S(stream);
+    if (cudaMemsetAsync(w.fix_count, 0, 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
+    int rc = launch_prep(k, B * Hkv, n_local, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, W, g.KL, w.NT,
+                         w.wt, w.wmax, w.status, st);
+    if (rc) return rc;
+    return launch_hash_gemm(w.xt, w.wt, w.xnorm, w.wmax, codes, w.fix_list, w.fix_count, w.fix_cap, B * Hkv,
+                            n_local, w.n_pad, g.nchunks, w.KD, g.KL, w.NT, g.KLq, w.status, nullptr, st);
+}
+
+int magicpig_build_index(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,
+                         const float* W, float* center, int64_t* r2, uint32_t* codes, int64_t* key_sum,
+                         int64_t* count, void* ws, size_t ws_bytes, void* stream) {
+    int rc = magicpig_key_stats(cfg, k, B, Hkv, n, 0, n, key_sum, count, ws, ws_bytes, stream);
+    if (rc) return rc;
+    rc = magicpig_key_norms(cfg, k, B, Hkv, n, 0, n, key_sum, count, center, r2, ws, ws_bytes, stream);
+    if (rc) return rc;
+    return magicpig_build_tables(cfg, k, B, Hkv, n, 0, n, W, center, r2, codes, ws, ws_bytes, stream);
+}
+
+int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64_t B, int64_t Hq, const float* W,
+                            void* ws, size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || B < 1 || Hq < 1 || !q || !W || !ws) return MAGICPIG_EINVAL;
+    // the query-code region sits at the same offset in every decode workspace
+    DecodeWs w = decode_layout(cfg, B, Hq, 1, 0, ws);
+    if (ws_bytes < 256 + (size_t)B * Hq * make_geom(cfg->K, cfg->L, 0).KLw * 4) return MAGICPIG_EWORKSPACE;
+    const Geom g = make_geom(cfg->K, cfg->L, 0);
+    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
+}
+
+int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
+                            const float* center, const int64_t* r2, const uint16_t* k, const uint16_t* v, int64_t B,
+                            int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
+                            float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
+                            void* stream) {
+    if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
+    if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
+    const int64_t G = Hq / Hkv;
+    if (G != 1 && G != 2 && G != 4 && G != 8) return MAGICPIG_EINVAL;
+    if (!q || !center || !r2 || !ws) return MAGICPIG_EINVAL;
+    if (n_local > 0 && (!codes || !k || !v)) return MAGICPIG_EINVAL;
+    DecodeWs w = decode_layout(cfg, B, Hq, Hkv, n_local, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    cudaStream_t st = S(stream);
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    if (n_local == 0) {
+        // nothing on this shard: empty partial states, zero outputs
+        if (partial) {
+            int rc0 = launch_empty_partial(partial, B * Hq, st);
+            if (rc0) return rc0;
+        }
+        if (out && cudaMemsetAsync(out, 0, (size_t)B * Hq * HD * 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
+        if (s_count && cudaMemsetAsync(s_count, 0, (size_t)B * Hq * 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
+        return MAGICPIG_OK;
+    }
+    DecodeArgs a;
+    memset(&a, 0, sizeof(a));
+    a.q = q;
+    a.qbits = w.qbits;
+    a.codes = codes;
+    a.center = center;
+    a.r2 = r2;
+    a.k = k;
+    a.v = v;
+    a.B = B;
+    a.Hkv = Hkv;
+    a.Hq = Hq;
+    a.n_local = n_local;
+    a.seq_offset = seq_offset;
+    a.n_global = n_global;
+    a.K = cfg->K;
+    a.L = cfg->L;
+    a.KL = g.KL;
+    a.KLw = g.KLw;
+    a.KLq = g.KLq;
+    a.ngroups = g.ngroups;
+    a.TG = g.TG;
+    a.QG = g.QG;
+    a.nchunks = g.nchunks;
+    const int64_t total = B * Hkv * g.nchunks;
+    int64_t ts = (4 * (int64_t)num_sms() + total - 1) / total;
+    int64_t tsmax = g.ngroups / (DEC_THREADS / 32);
+    if (tsmax < 1) tsmax = 1;
+    if (ts > tsmax) ts = tsmax;
+    if (ts < 1) ts = 1;
+    a.tsplit = (int)ts;
+    a.sink = cfg->sink;
+    a.local = cfg->local;
+    a.minc = cfg->min_collisions;
+    a.mips = cfg->mips;
+    a.out = out;
+    a.partial = partial;
+    a.s_count = s_count;
+    a.s_mask = s_mask;
+    a.seen = w.seen;
+    a.chunk_ctr = w.chunk_ctr;
+    a.unit_ctr = w.unit_ctr;
+    a.parts = w.parts;
+    a.chunk_cnt = w.chunk_cnt;
+    a.status = w.status;
+    return launch_decode(a, st);
+}
+
+int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
+                    const float* center, const int64_t* r2, const uint16_t* k, const uint16_t* v, int64_t B,
+                    int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, const float* W, float* out,
+                    float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes, void* stream) {
+    if (!W) return MAGICPIG_EINVAL;
+    if (n_local > 0) {
+        int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
+        if (rc) return rc;
+    }
+    return magicpig_decode_encoded(cfg, q, Hq, codes, center, r2, k, v, B, Hkv, n_local, seq_offset, n_global, out,
+                                   partial, s_count, s_mask, ws, ws_bytes, stream);
+}
+
+int magicpig_merge_partials(const float* parts, int P, int64_t BH, float* out, void* stream) {
+    if (!parts || !out || P < 1 || BH < 1) return MAGICPIG_EINVAL;
+    return launch_merge(parts, P, BH, out, S(stream));
+}
+
+int magicpig_export_codes(const magicpig_config* cfg, const uint32_t* codes, int64_t B, int64_t Hkv,
+                          int64_t n_local, uint16_t* canonical, void* stream) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || n_local < 0 || (n_local > 0 && (!codes || !canonical)))
+        return MAGICPIG_EINVAL;
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    return launch_export_codes(codes, B * Hkv, n_local, cfg->K, cfg->L, g.KLq, g.nchunks, canonical, S(stream));
+}
+
+int magicpig_import_codes(const magicpig_config* cfg, const uint16_t* canonical, int64_t B, int64_t Hkv,
+                          int64_t n_local, uint32_t* codes, void* stream) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || n_local < 0 || (n_local > 0 && (!codes || !canonical)))
+        return MAGICPIG_EINVAL;
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    return launch_import_codes(canonical, B * Hkv, n_local, cfg->K, cfg->L, g.KLq, g.nchunks, codes, S(stream));
+}
+
+int magicpig_query_codes(const magicpig_config* cfg, const uint16_t* q, int64_t B, int64_t Hq, const float* W,
+                         uint16_t* qcodes, void* ws, size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || B < 1 || Hq < 1 || !q || !W || !qcodes || !ws) return MAGICPIG_EINVAL;
+    DecodeWs w = decode_layout(cfg, B, Hq, 1, 0, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    const Geom g = make_geom(cfg->K, cfg->L, 0);
+    int rc = launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
+    if (rc) return rc;
+    return launch_qbits_to_canonical(w.qbits, B * Hq, cfg->K, cfg->L, g.KLw, qcodes, S(stream));
+}
+
+int magicpig_collision_counts(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
+                              int64_t B, int64_t Hkv, int64_t n_local, const float* W, uint16_t* counts, void* ws,
+                              size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || Hq < Hkv || Hq % Hkv || n_local < 0) return MAGICPIG_EINVAL;
+    if (!q || !W || !ws || (n_local > 0 && (!codes || !counts))) return MAGICPIG_EINVAL;
+    DecodeWs w = decode_layout(cfg, B, Hq, Hkv, n_local, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    int rc = launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
+    if (rc) return rc;
+    return launch_collision_counts(w.qbits, codes, B, Hkv, Hq, n_local, cfg->K, cfg->L, g.KLw, g.KLq, g.nchunks,
+                                   counts, S(stream));
+}
+
+int magicpig_debug_hash_acc(const magicpig_config* cfg, const uint16_t* k, int64_t n_local, const float* W,
+                            const float* center, const int64_t* r2, float* acc, void* ws, size_t ws_bytes,
+                            void* stream) {
+    if (!cfg_ok(cfg) || n_local < 1 || !k || !W || !center || !r2 || !acc || !ws) return MAGICPIG_EINVAL;
+    BuildWs w = build_layout(cfg, 1, 1, n_local, ws);
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    size_t codes_bytes = (size_t)g.nchunks * g.KLq * 128 * 4;
+    if (ws_bytes < w.bytes + align256(codes_bytes)) return MAGICPIG_EWORKSPACE;
+    uint32_t* scratch_codes = (uint32_t*)((uint8_t*)ws + w.bytes);
+    cudaStream_t st = S(stream);
+    if (cudaMemsetAsync(w.fix_count, 0, 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
+    int rc = launch_prep(k, 1, n_local, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, W, g.KL, w.NT, w.wt,
+                         w.wmax, w.status, st);
+    if (rc) return rc;
+    return launch_hash_gemm(w.xt, w.wt, w.xnorm, w.wmax, scratch_codes, w.fix_list, w.fix_count, w.fix_cap, 1,
+                            n_local, w.n_pad, g.nchunks, w.KD, g.KL, w.NT, g.KLq, w.status, acc, st);
+}
+
+const char* magicpig_strerror(int err) {
+    switch (err) {
+        case MAGICPIG_OK: return "ok";
+        case MAGICPIG_EINVAL: return "invalid argument (shape, range or NULL pointer)";
+        case MAGICPIG_ENOTREPR: return "projection value not bf16-representable";
+        case MAGICPIG_EDEGENERATE: return "a head had neither sampled nor static keys";
+        case MAGICPIG_ECUDA: return "CUDA error";
+        case MAGICPIG_EWORKSPACE: return "workspace too small";
+        case MAGICPIG_EINEXACT: return "value outside the exact fixed-point range (|k| >= 2^27)";
+        case MAGICPIG_EOVERFLOW: return "hash fix-up list overflow";
+    }
+    return "unknown error";
+}
+
+const char* magicpig_version(void) { return "magicpig-b200 0.1 (sm_100a)"; }
+
+uint64_t magicpig_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// kernels.cuh -- internal launcher declarations (CUDA path only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mp {
+
+constexpr int STATS_SPLIT = 1024;  // keys per partial-statistics CTA
+constexpr int DEC_THREADS = 256;   // decode CTA (8 warps)
+
+void count_launch(int n);
+size_t gemm_smem_bytes(int KD);
+
+int launch_key_stats(const uint16_t* k, int64_t units, int64_t n_local, int64_t seq_offset, int64_t n_global,
+                     int sink, int local, int64_t* part_sum, int64_t* part_cnt, int64_t* key_sum,
+                     int64_t* count, uint32_t* status, cudaStream_t st);
+int launch_key_norms(const uint16_t* k, int64_t units, int64_t n_local, int64_t seq_offset, int64_t n_global,
+                     int sink, int local, int do_center, const int64_t* key_sum, const int64_t* count,
+                     float* center, int64_t* part_r2, int64_t* r2, uint32_t* status, cudaStream_t st);
+int launch_reduce_shards(int mode, const int64_t* parts_sum, const int64_t* parts_cnt, int P, int64_t units,
+                         int64_t* out_sum, int64_t* out_cnt, cudaStream_t st);
+int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad, int mips, int KD,
+                const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, const float* W, int KL,
+                int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st);
+int launch_hash_gemm(const uint8_t* xt, const uint8_t* wt, const float* xnorm, const float* wmax,
+                     uint32_t* codes, uint2* fix_list, uint32_t* fix_count, uint32_t fix_cap, int64_t units,
+                     int64_t n_local, int64_t n_pad, int64_t nchunks, int KD, int KL, int NT, int KLq,
+                     uint32_t* status, float* dbg_acc, cudaStream_t st);
+
+int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
+                   uint32_t* status, cudaStream_t st);
+
+struct DecodeArgs {
+    const uint16_t* q;
+    const uint32_t* qbits;
+    const uint32_t* codes;
+    const float* center;
+    const int64_t* r2;
+    const uint16_t* k;
+    const uint16_t* v;
+    int64_t B, Hkv, Hq, n_local, seq_offset, n_global;
+    int K, L, KL, KLw, KLq, ngroups, TG, QG;
+    int64_t nchunks;
+    int tsplit, sink, local, minc, mips;
+    float* out;
+    float* partial;
+    int32_t* s_count;
+    uint32_t* s_mask;
+    uint32_t* seen;
+    uint32_t* chunk_ctr;
+    uint32_t* unit_ctr;
+    float* parts;
+    int32_t* chunk_cnt;
+    uint32_t* status;
+};
+int launch_decode(const DecodeArgs& a, cudaStream_t st);
+int launch_merge(const float* parts, int P, int64_t BH, float* out, cudaStream_t st);
+int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st);
+
+int launch_export_codes(const uint32_t* codes, int64_t units, int64_t n_local, int K, int L, int KLq,
+                        int64_t nchunks, uint16_t* canonical, cudaStream_t st);
+int launch_import_codes(const uint16_t* canonical, int64_t units, int64_t n_local, int K, int L, int KLq,
+                        int64_t nchunks, uint32_t* codes, cudaStream_t st);
+int launch_qbits_to_canonical(const uint32_t* qbits, int64_t BHq, int K, int L, int KLw, uint16_t* out,
+                              cudaStream_t st);
+int launch_collision_counts(const uint32_t* qbits, const uint32_t* codes, int64_t B, int64_t Hkv, int64_t Hq,
+                            int64_t n_local, int K, int L, int KLw, int KLq, int64_t nchunks, uint16_t* counts,
+                            cudaStream_t st);
+
+}  // namespace mp

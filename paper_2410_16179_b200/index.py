@@ -1,0 +1,141 @@
+"""MagicPIG index: device buffers + the build / decode sequence over the C ABI,
+including multi-GPU sharding with torch.distributed (NCCL on GPUs).
+
+Sharding:
+  * heads / batch: each rank owns whole (sequence, kv head) units -> no
+    collective on the data path (weak scaling);
+  * sequence: each rank owns a contiguous key range.  Build: all-gather of the
+    exact fixed-point centering sums (summed exactly on device), then of the
+    per-shard MIPS radius (max on device) -> every rank hashes with the global
+    c and r, so the union of the shards' S is the unsharded S.  Decode: each
+    rank emits (m, s, a) partial states; one all-gather; the same fixed-order
+    log-sum-exp merge on every rank ("recursive attention").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import binding as B_
+
+
+@dataclass
+class IndexBuffers:
+    center: torch.Tensor   # [B][Hkv][128] f32
+    r2: torch.Tensor       # [B][Hkv][2] int64 (q64)
+    codes: torch.Tensor    # [codes_words] int32 (uint32 bit planes)
+    key_sum: torch.Tensor  # [B][Hkv][128][2] int64 (q64)
+    count: torch.Tensor    # [B][Hkv] int64
+
+
+class MagicPIG:
+    """One attention layer's LSH index over a KV cache k, v [B][Hkv][n][128] bf16."""
+
+    def __init__(self, W: torch.Tensor, K=10, L=150, center=1, mips=1, min_collisions=2, sink=4, local=64):
+        self.cfg = B_.make_config(K, L, center, mips, min_collisions, sink, local)
+        rc = B_.lib().magicpig_validate_config(B_.C.byref(self.cfg))
+        if rc != 0:
+            raise B_.MagicPIGError("unsupported configuration")
+        if W.dtype != torch.float32 or not W.is_cuda:
+            raise B_.MagicPIGError("W must be a CUDA float32 tensor [(128+mips)][K*L]")
+        if tuple(W.shape) != (128 + (1 if mips else 0), K * L):
+            raise B_.MagicPIGError(f"W shape {tuple(W.shape)} != {(128 + mips, K * L)}")
+        self.W = W.contiguous()
+        self.buf: Optional[IndexBuffers] = None
+        self._ws_build = None
+        self._ws_dec = None
+        self.seq_offset = 0
+        self.n_global = 0
+        self.shape = None
+
+    # ------------------------------------------------------------ helpers
+    def _alloc(self, Bn, Hkv, n, dev):
+        words = B_.codes_words(self.cfg, Bn, Hkv, n)
+        self.buf = IndexBuffers(
+            center=torch.empty((Bn, Hkv, 128), dtype=torch.float32, device=dev),
+            r2=torch.empty((Bn, Hkv, 2), dtype=torch.int64, device=dev),
+            codes=torch.empty((max(words, 1),), dtype=torch.int32, device=dev),
+            key_sum=torch.empty((Bn, Hkv, 128, 2), dtype=torch.int64, device=dev),
+            count=torch.empty((Bn, Hkv), dtype=torch.int64, device=dev))
+        nb = B_.build_workspace_bytes(self.cfg, Bn, Hkv, n)
+        if self._ws_build is None or self._ws_build.numel() < nb:
+            self._ws_build = B_.new_workspace(nb, dev)
+
+    def decode_workspace(self, Bn, Hq, Hkv, n, dev):
+        nb = B_.decode_workspace_bytes(self.cfg, Bn, Hq, Hkv, n)
+        if self._ws_dec is None or self._ws_dec.numel() < nb:
+            self._ws_dec = B_.new_workspace(nb, dev)
+        return self._ws_dec
+
+    def release_build_workspace(self):
+        self._ws_build = None
+
+    # ------------------------------------------------------------ build
+    def build(self, k: torch.Tensor):
+        """Unsharded build over k [B][Hkv][n][128] bf16."""
+        Bn, Hkv, n, d = k.shape
+        self._alloc(Bn, Hkv, n, k.device)
+        b = self.buf
+        B_.build_index(self.cfg, k, self.W, b.center, b.r2, b.codes, b.key_sum, b.count, self._ws_build)
+        self.seq_offset, self.n_global, self.shape = 0, n, (Bn, Hkv, n)
+        return self
+
+    def build_sharded(self, k_local: torch.Tensor, seq_offset: int, n_global: int, group=None):
+        """Sequence-sharded build: this rank holds keys [seq_offset, seq_offset + n_local)."""
+        import torch.distributed as dist
+        Bn, Hkv, n, d = k_local.shape
+        self._alloc(Bn, Hkv, n, k_local.device)
+        b = self.buf
+        ws = self._ws_build
+        P = dist.get_world_size(group)
+        ks = torch.empty_like(b.key_sum)
+        cnt = torch.empty_like(b.count)
+        B_.key_stats(self.cfg, k_local, seq_offset, n_global, ks, cnt, ws)
+        all_ks = torch.empty((P,) + tuple(ks.shape), dtype=ks.dtype, device=ks.device)
+        all_cnt = torch.empty((P,) + tuple(cnt.shape), dtype=cnt.dtype, device=cnt.device)
+        dist.all_gather_into_tensor(all_ks, ks.contiguous(), group=group)
+        dist.all_gather_into_tensor(all_cnt, cnt.contiguous(), group=group)
+        B_.reduce_stats(0, all_ks, all_cnt, P, Bn, Hkv, b.key_sum, b.count)
+        r2_local = torch.empty_like(b.r2)
+        B_.key_norms(self.cfg, k_local, seq_offset, n_global, b.key_sum, b.count, b.center, r2_local, ws)
+        all_r2 = torch.empty((P,) + tuple(r2_local.shape), dtype=r2_local.dtype, device=r2_local.device)
+        dist.all_gather_into_tensor(all_r2, r2_local.contiguous(), group=group)
+        B_.reduce_stats(1, all_r2, None, P, Bn, Hkv, b.r2, None)
+        B_.build_tables(self.cfg, k_local, seq_offset, n_global, self.W, b.center, b.r2, b.codes, ws)
+        self.seq_offset, self.n_global, self.shape = seq_offset, n_global, (Bn, Hkv, n)
+        return self
+
+    # ------------------------------------------------------------ decode
+    def decode(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out=None, partial=None,
+               s_count=None, s_mask=None):
+        """One decode step for q [B][Hq][128] bf16 over this rank's keys."""
+        Bn, Hkv, n, _ = k.shape
+        Hq = q.shape[1]
+        ws = self.decode_workspace(Bn, Hq, Hkv, n, q.device)
+        if out is None and partial is None:
+            out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=q.device)
+        b = self.buf
+        B_.decode(self.cfg, q, b.codes, b.center, b.r2, k, v, self.seq_offset, self.n_global, self.W, ws,
+                  out=out, partial=partial, s_count=s_count, s_mask=s_mask)
+        return out if out is not None else partial
+
+    def decode_sharded(self, q, k_local, v_local, group=None, out=None, s_count=None):
+        """Sequence-sharded decode: partial states, one all-gather, fixed-order merge."""
+        import torch.distributed as dist
+        Bn, Hkv, n, _ = k_local.shape
+        Hq = q.shape[1]
+        P = dist.get_world_size(group)
+        part = torch.empty((Bn * Hq, B_.PART), dtype=torch.float32, device=q.device)
+        self.decode(q, k_local, v_local, partial=part, s_count=s_count)
+        allp = torch.empty((P, Bn * Hq, B_.PART), dtype=torch.float32, device=q.device)
+        dist.all_gather_into_tensor(allp, part, group=group)
+        if out is None:
+            out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=q.device)
+        B_.merge_partials(allp, out)
+        return out
+
+    def status(self, which="decode") -> int:
+        ws = self._ws_dec if which == "decode" else self._ws_build
+        return B_.workspace_status(ws) if ws is not None else 0

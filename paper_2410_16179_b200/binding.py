@@ -67,8 +67,9 @@ _SIGS = {
 _lib = None
 
 
-def lib(load_only: bool = False):
-    """Load the in-tree shared library (building it if stale)."""
+def lib(load_only: bool = True):
+    """Load the in-tree shared library (building it only if it is missing, or
+    if stale when load_only=False)."""
     global _lib
     if _lib is None:
         path = _build.LIB

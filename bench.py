@@ -213,7 +213,7 @@ def run_ours(args):
     nw = (n + 31) // 32
     smask = torch.zeros((Bn, Hq, nw), dtype=torch.int32, device=dev)
     scount = torch.zeros((Bn, Hq), dtype=torch.int32, device=dev)
-    B_.decode(cfg, qs[0], mps[0].buf.codes, mps[0].buf.center, mps[0].buf.r2, ks[0], vs[0], 0, n, tW, ws,
+    B_.decode(cfg, qs[0], mps[0].buf.codes, mps[0].buf.center, mps[0].buf.key_norm, ks[0], vs[0], 0, n, tW, ws,
               out=outs[0], s_count=scount, s_mask=smask)
     torch.cuda.synchronize()
     status = B_.workspace_status(ws)
@@ -224,7 +224,7 @@ def run_ours(args):
     nD = n - nT
     KL = wl.K * wl.L
     bytes_codes = Bn * Hkv * nD * KL / 8
-    bytes_rows = (n_union + Bn * Hkv * nT) * 512
+    bytes_rows = (n_union + Bn * Hkv * nT) * 512 + n_union * 4  # K/V rows + |xbar_i| of sampled keys
     bytes_misc = Bn * Hq * (256 + KL / 8) + Bn * Hkv * 512
     alg_bytes = bytes_codes + bytes_rows + bytes_misc
     sampled_frac = float(scount.float().mean().item()) / max(nD, 1)
@@ -233,11 +233,11 @@ def run_ours(args):
 
     def step(r):
         B_.encode_queries(cfg, qs[r], tW, ws)
-        B_.decode_encoded(cfg, qs[r], mps[r].buf.codes, mps[r].buf.center, mps[r].buf.r2, ks[r], vs[r], 0, n, ws,
+        B_.decode_encoded(cfg, qs[r], mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n, ws,
                           out=outs[r])
 
     def kernel_only(r):
-        B_.decode_encoded(cfg, qs[r], mps[r].buf.codes, mps[r].buf.center, mps[r].buf.r2, ks[r], vs[r], 0, n, ws,
+        B_.decode_encoded(cfg, qs[r], mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n, ws,
                           out=outs[r])
 
     def capture(fn, nsteps, offset=0):

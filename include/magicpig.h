@@ -130,17 +130,20 @@ int magicpig_reduce_stats(int mode, const int64_t* parts_sum, const int64_t* par
  *     by all heads.  Row 128 multiplies the MIPS coordinate.
  *   codes: magicpig_codes_words() uint32, bit-plane layout above.  Bit =
  *     [exact(xbar_i . W_j) > 0] (R6), xbar_i = [x_i, s_i] (s_i with mips).
+ *   key_norm[B][Hkv][n_local] fp32: |xbar_i| = sqrt(fl64(n2q 2^-64) + s_i^2),
+ *     the norm of the hashed key vector used for p_i at decode (R5).
  * Runs on tcgen05 tensor cores (fp32 accumulate) with an error-bound filter
  * and exact integer fix-up of every near-zero dot, so bits are exact. */
 int magicpig_build_tables(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv,
                           int64_t n_local, int64_t seq_offset, int64_t n_global, const float* W,
-                          const float* center, const int64_t* r2, uint32_t* codes, void* ws,
-                          size_t ws_bytes, void* stream);
+                          const float* center, const int64_t* r2, uint32_t* codes, float* key_norm,
+                          void* ws, size_t ws_bytes, void* stream);
 
 /* All three phases for an unsharded cache (seq_offset = 0, n_global = n). */
 int magicpig_build_index(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv,
                          int64_t n, const float* W, float* center, int64_t* r2, uint32_t* codes,
-                         int64_t* key_sum, int64_t* count, void* ws, size_t ws_bytes, void* stream);
+                         float* key_norm, int64_t* key_sum, int64_t* count, void* ws, size_t ws_bytes,
+                         void* stream);
 
 /* --------------------------------------------------------------- decode ---
  * One MagicPIG decode step (Alg. 1) for all B x Hq query heads:
@@ -156,9 +159,9 @@ int magicpig_build_index(const magicpig_config* cfg, const uint16_t* k, int64_t 
  *   s_count[B][Hq]       |S_g| on this shard (NULL to skip)
  *   s_mask[B][Hq][ceil(n_local/32)]  debug: bit r of word w = key 32w+r in S_g
  *                        (NULL to skip; costs extra stores)
- * center, r2: from the build.  W: same array as the build.             */
+ * center, key_norm: from the build.  W: same array as the build.       */
 int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
-                    const float* center, const int64_t* r2, const uint16_t* k, const uint16_t* v,
+                    const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v,
                     int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global,
                     const float* W, float* out, float* partial, int32_t* s_count, uint32_t* s_mask,
                     void* ws, size_t ws_bytes, void* stream);
@@ -170,7 +173,7 @@ int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, c
 int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64_t B, int64_t Hq,
                             const float* W, void* ws, size_t ws_bytes, void* stream);
 int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
-                            const uint32_t* codes, const float* center, const int64_t* r2,
+                            const uint32_t* codes, const float* center, const float* key_norm,
                             const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
                             int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
                             float* partial, int32_t* s_count, uint32_t* s_mask, void* ws,
@@ -197,6 +200,7 @@ int magicpig_collision_counts(const magicpig_config* cfg, const uint16_t* q, int
                               void* stream);
 /* Raw fp32 tensor-core accumulators of the hash GEMM for the first
  * min(n_local, 128) keys of unit 0 and all K*L columns: acc[128][K*L]
+ * (workspace: build workspace + 4*codes_words + 4*n_local bytes, 256-aligned)
  * (measures the tcgen05 accumulation error that the fix-up filter bounds). */
 int magicpig_debug_hash_acc(const magicpig_config* cfg, const uint16_t* k, int64_t n_local,
                             const float* W, const float* center, const int64_t* r2, float* acc,

@@ -46,8 +46,8 @@ _SIGS = {
     "magicpig_key_stats": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _sz, _p], _i),
     "magicpig_key_norms": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
     "magicpig_reduce_stats": ([_i, _p, _p, _i, _i64, _i64, _p, _p, _p], _i),
-    "magicpig_build_tables": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
-    "magicpig_build_index": ([_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_build_tables": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_build_index": ([_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p], _i),
     "magicpig_decode": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p,
                          _p, _sz, _p], _i),
     "magicpig_encode_queries": ([_p, _p, _i64, _i64, _p, _p, _sz, _p], _i),
@@ -163,26 +163,26 @@ def reduce_stats(mode, parts_sum, parts_cnt, P, B, Hkv, out_sum, out_cnt):
                                        _ptr(out_cnt), _stream()), "reduce_stats")
 
 
-def build_tables(cfg, k, seq_offset, n_global, W, center, r2, codes, ws):
+def build_tables(cfg, k, seq_offset, n_global, W, center, r2, codes, key_norm, ws):
     B, Hkv, n, _ = k.shape
     _check(lib().magicpig_build_tables(_cfg(cfg), _ptr(k), B, Hkv, n, seq_offset, n_global, _ptr(W),
-                                       _ptr(center), _ptr(r2), _ptr(codes), _ptr(ws), ws.numel(), _stream()),
-           "build_tables")
+                                       _ptr(center), _ptr(r2), _ptr(codes), _ptr(key_norm), _ptr(ws), ws.numel(),
+                                       _stream()), "build_tables")
 
 
-def build_index(cfg, k, W, center, r2, codes, key_sum, count, ws):
+def build_index(cfg, k, W, center, r2, codes, key_norm, key_sum, count, ws):
     B, Hkv, n, _ = k.shape
     _check(lib().magicpig_build_index(_cfg(cfg), _ptr(k), B, Hkv, n, _ptr(W), _ptr(center), _ptr(r2),
-                                      _ptr(codes), _ptr(key_sum), _ptr(count), _ptr(ws), ws.numel(), _stream()),
-           "build_index")
+                                      _ptr(codes), _ptr(key_norm), _ptr(key_sum), _ptr(count), _ptr(ws), ws.numel(),
+                                      _stream()), "build_index")
 
 
 # ---------------------------------------------------------------- decode
-def decode(cfg, q, codes, center, r2, k, v, seq_offset, n_global, W, ws, out=None, partial=None,
+def decode(cfg, q, codes, center, key_norm, k, v, seq_offset, n_global, W, ws, out=None, partial=None,
            s_count=None, s_mask=None):
     B, Hkv, n, _ = k.shape
     Hq = q.shape[1]
-    _check(lib().magicpig_decode(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(r2), _ptr(k), _ptr(v),
+    _check(lib().magicpig_decode(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(key_norm), _ptr(k), _ptr(v),
                                  B, Hkv, n, seq_offset, n_global, _ptr(W), _ptr(out), _ptr(partial),
                                  _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(), _stream()), "decode")
 
@@ -193,11 +193,11 @@ def encode_queries(cfg, q, W, ws):
            "encode_queries")
 
 
-def decode_encoded(cfg, q, codes, center, r2, k, v, seq_offset, n_global, ws, out=None, partial=None,
+def decode_encoded(cfg, q, codes, center, key_norm, k, v, seq_offset, n_global, ws, out=None, partial=None,
                    s_count=None, s_mask=None):
     Bn, Hkv, n, _ = k.shape
     Hq = q.shape[1]
-    _check(lib().magicpig_decode_encoded(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(r2), _ptr(k),
+    _check(lib().magicpig_decode_encoded(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(key_norm), _ptr(k),
                                          _ptr(v), Bn, Hkv, n, seq_offset, n_global, _ptr(out), _ptr(partial),
                                          _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(), _stream()),
            "decode_encoded")

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) prep_x_kernel(const uint16_t* __restrict_
                                                      const float* __restrict__ center,
                                                      const int64_t* __restrict__ r2,
                                                      uint8_t* __restrict__ xt, float* __restrict__ xnorm,
-                                                     uint32_t* status) {
+                                                     float* __restrict__ key_norm, uint32_t* status) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t unit = blockIdx.y;
     const int64_t i = (int64_t)blockIdx.x * 8 + warp;
@@ -226,10 +226,14 @@ __global__ void __launch_bounds__(256) prep_x_kernel(const uint16_t* __restrict_
         *reinterpret_cast<uint4*>(tbase + (16 + lane) * 16 * 128 + rowoff) = v;
         if (lane == 0) {
             float sf = bf2f(s);
-            xnorm[unit * n_pad + i] = i < n_local ? (float)sqrt(n2d + (double)sf * (double)sf) : -1.0f;
+            float nr = (float)sqrt(n2d + (double)sf * (double)sf);
+            xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
+            if (i < n_local) key_norm[unit * n_local + i] = nr;
         }
     } else if (KD == HD && lane == 0) {
-        xnorm[unit * n_pad + i] = i < n_local ? (float)sqrt(q64_to_double((i128)n2)) : -1.0f;
+        float nr = (float)sqrt(q64_to_double((i128)n2));
+        xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
+        if (i < n_local) key_norm[unit * n_local + i] = nr;
     }
 }
 
@@ -314,11 +318,11 @@ int launch_reduce_shards(int mode, const int64_t* parts_sum, const int64_t* part
 }
 
 int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad, int mips, int KD,
-                const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, const float* W, int KL,
-                int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st) {
+                const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, float* key_norm, const float* W,
+                int KL, int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st) {
     cudaMemsetAsync(wmax, 0, sizeof(float), st);
     prep_x_kernel<<<dim3((unsigned)((n_pad + 7) / 8), (unsigned)units), 256, 0, st>>>(
-        k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, status);
+        k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, key_norm, status);
     prep_w_kernel<<<NT, 64, 0, st>>>(W, HD + (mips ? 1 : 0), KL, KD, wt, wmax, status);
     count_launch(2);
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;

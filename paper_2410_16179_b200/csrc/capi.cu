@@ -204,30 +204,31 @@ int magicpig_reduce_stats(int mode, const int64_t* parts_sum, const int64_t* par
 
 int magicpig_build_tables(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n_local,
                           int64_t seq_offset, int64_t n_global, const float* W, const float* center,
-                          const int64_t* r2, uint32_t* codes, void* ws, size_t ws_bytes, void* stream) {
+                          const int64_t* r2, uint32_t* codes, float* key_norm, void* ws, size_t ws_bytes,
+                          void* stream) {
     if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
-    if (!W || !center || !r2 || !codes || !ws || (n_local > 0 && !k)) return MAGICPIG_EINVAL;
+    if (!W || !center || !r2 || !codes || !ws || (n_local > 0 && (!k || !key_norm))) return MAGICPIG_EINVAL;
     BuildWs w = build_layout(cfg, B, Hkv, n_local, ws);
     if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
     if (n_local == 0) return MAGICPIG_OK;
     const Geom g = make_geom(cfg->K, cfg->L, n_local);
     cudaStream_t st = S(stream);
     if (cudaMemsetAsync(w.fix_count, 0, 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
-    int rc = launch_prep(k, B * Hkv, n_local, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, W, g.KL, w.NT,
-                         w.wt, w.wmax, w.status, st);
+    int rc = launch_prep(k, B * Hkv, n_local, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, key_norm, W,
+                         g.KL, w.NT, w.wt, w.wmax, w.status, st);
     if (rc) return rc;
     return launch_hash_gemm(w.xt, w.wt, w.xnorm, w.wmax, codes, w.fix_list, w.fix_count, w.fix_cap, B * Hkv,
                             n_local, w.n_pad, g.nchunks, w.KD, g.KL, w.NT, g.KLq, w.status, nullptr, st);
 }
 
 int magicpig_build_index(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,
-                         const float* W, float* center, int64_t* r2, uint32_t* codes, int64_t* key_sum,
-                         int64_t* count, void* ws, size_t ws_bytes, void* stream) {
+                         const float* W, float* center, int64_t* r2, uint32_t* codes, float* key_norm,
+                         int64_t* key_sum, int64_t* count, void* ws, size_t ws_bytes, void* stream) {
     int rc = magicpig_key_stats(cfg, k, B, Hkv, n, 0, n, key_sum, count, ws, ws_bytes, stream);
     if (rc) return rc;
     rc = magicpig_key_norms(cfg, k, B, Hkv, n, 0, n, key_sum, count, center, r2, ws, ws_bytes, stream);
     if (rc) return rc;
-    return magicpig_build_tables(cfg, k, B, Hkv, n, 0, n, W, center, r2, codes, ws, ws_bytes, stream);
+    return magicpig_build_tables(cfg, k, B, Hkv, n, 0, n, W, center, r2, codes, key_norm, ws, ws_bytes, stream);
 }
 
 int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64_t B, int64_t Hq, const float* W,
@@ -241,7 +242,7 @@ int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64
 }
 
 int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
-                            const float* center, const int64_t* r2, const uint16_t* k, const uint16_t* v, int64_t B,
+                            const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B,
                             int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
                             float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
                             void* stream) {
@@ -249,7 +250,8 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
     if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
     const int64_t G = Hq / Hkv;
     if (G != 1 && G != 2 && G != 4 && G != 8) return MAGICPIG_EINVAL;
-    if (!q || !center || !r2 || !ws) return MAGICPIG_EINVAL;
+    if (!q || !center || !ws) return MAGICPIG_EINVAL;
+    if (n_local > 0 && !key_norm) return MAGICPIG_EINVAL;
     if (n_local > 0 && (!codes || !k || !v)) return MAGICPIG_EINVAL;
     DecodeWs w = decode_layout(cfg, B, Hq, Hkv, n_local, ws);
     if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
@@ -271,7 +273,7 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
     a.qbits = w.qbits;
     a.codes = codes;
     a.center = center;
-    a.r2 = r2;
+    a.key_norm = key_norm;
     a.k = k;
     a.v = v;
     a.B = B;
@@ -299,7 +301,6 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
     a.sink = cfg->sink;
     a.local = cfg->local;
     a.minc = cfg->min_collisions;
-    a.mips = cfg->mips;
     a.out = out;
     a.partial = partial;
     a.s_count = s_count;
@@ -314,7 +315,7 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
 }
 
 int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
-                    const float* center, const int64_t* r2, const uint16_t* k, const uint16_t* v, int64_t B,
+                    const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B,
                     int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, const float* W, float* out,
                     float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes, void* stream) {
     if (!W) return MAGICPIG_EINVAL;
@@ -322,7 +323,7 @@ int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, c
         int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
         if (rc) return rc;
     }
-    return magicpig_decode_encoded(cfg, q, Hq, codes, center, r2, k, v, B, Hkv, n_local, seq_offset, n_global, out,
+    return magicpig_decode_encoded(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
                                    partial, s_count, s_mask, ws, ws_bytes, stream);
 }
 
@@ -379,12 +380,13 @@ int magicpig_debug_hash_acc(const magicpig_config* cfg, const uint16_t* k, int64
     BuildWs w = build_layout(cfg, 1, 1, n_local, ws);
     const Geom g = make_geom(cfg->K, cfg->L, n_local);
     size_t codes_bytes = (size_t)g.nchunks * g.KLq * 128 * 4;
-    if (ws_bytes < w.bytes + align256(codes_bytes)) return MAGICPIG_EWORKSPACE;
+    if (ws_bytes < w.bytes + align256(codes_bytes) + align256((size_t)n_local * 4)) return MAGICPIG_EWORKSPACE;
     uint32_t* scratch_codes = (uint32_t*)((uint8_t*)ws + w.bytes);
     cudaStream_t st = S(stream);
     if (cudaMemsetAsync(w.fix_count, 0, 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
-    int rc = launch_prep(k, 1, n_local, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, W, g.KL, w.NT, w.wt,
-                         w.wmax, w.status, st);
+    float* scratch_norm = (float*)((uint8_t*)ws + w.bytes + align256(codes_bytes));
+    int rc = launch_prep(k, 1, n_local, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, scratch_norm, W, g.KL,
+                         w.NT, w.wt, w.wmax, w.status, st);
     if (rc) return rc;
     return launch_hash_gemm(w.xt, w.wt, w.xnorm, w.wmax, scratch_codes, w.fix_list, w.fix_count, w.fix_cap, 1,
                             n_local, w.n_pad, g.nchunks, w.KD, g.KL, w.NT, g.KLq, w.status, acc, st);

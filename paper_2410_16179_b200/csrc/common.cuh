@@ -182,36 +182,43 @@ __device__ inline int exact_dot_sign_bf16(const uint16_t* a, const uint16_t* b, 
 }
 
 // --------------------------------------------------------------------------
-// sampling probability (Eq. LSH sampling probability), log u.
-// x = p^K;  min 2: u = P[Binomial(L, x) >= 2];  min 1: 1 - (1 - x)^L.
-// Evaluated without cancellation: for (L-1)x <= 1 the binomial tail term by
-// term, else 1 - exp((L-1) log1p(-x) + log1p((L-1)x)).  Double precision.
-__device__ inline double log_sampling_prob(double p, int K, int L, int minc) {
-    double x = pow(p, (double)K);
-    double u;
+// log of the sampling probability (Eq. LSH sampling probability):
+//   x = p^K;  min 2: u = P[Binomial(L, x) >= 2] = 1-(1-x)^L-Lx(1-x)^(L-1)
+//             min 1: u = 1-(1-x)^L
+// fp32 and cancellation-free (R11):
+//   y = (L-1) x <= 1:  ln u = ln C(L,2) + 2 ln x + (L-2) ln(1-x) + ln(1 + s),
+//                      s = sum_{j>=3} t_j/t_2 (Horner; t_{j+1}/t_j = (L-j)/(j+1) * x/(1-x))
+//   y > 1:             ln u = ln(-expm1((L-1) ln(1-x) + ln(1+y)))   (u >= 0.26)
+// floored at ln(1e-300).
+constexpr float LOG_U_FLOOR = -690.7755279f;
+
+__device__ __forceinline__ float log_sampling_prob(float p, int K, int L, int minc) {
+    if (!(p > 0.0f)) return LOG_U_FLOOR;
+    if (p >= 1.0f) return 0.0f;
+    const float lnx = (float)K * logf(p);
+    const float x = expf(lnx);
+    float lu;
     if (minc == 1) {
-        u = -expm1((double)L * log1p(-x));
-    } else if (x >= 1.0) {
-        u = 1.0;
-    } else if (x <= 0.0) {
-        u = 0.0;
+        const float Lx = (float)L * x;
+        if (Lx < 1e-4f) lu = lnx + logf((float)L) - 0.5f * (float)(L - 1) * x;
+        else lu = logf(-expm1f((float)L * log1pf(-x)));
     } else {
-        double y = (double)(L - 1) * x;
-        if (y > 1.0) {
-            u = -expm1((double)(L - 1) * log1p(-x) + log1p(y));
-        } else {
-            double r = x / (1.0 - x);
-            double term = 0.5 * (double)L * (double)(L - 1) * x * x * exp((double)(L - 2) * log1p(-x));
-            u = 0.0;
-            for (int j = 2; j <= L; j++) {
-                u += term;
-                if (term <= 1e-18 * u) break;
-                term *= r * (double)(L - j) / (double)(j + 1);
+        const float y = (float)(L - 1) * x;
+        if (y <= 1.0f) {
+            const float r = x / (1.0f - x);
+            float s = 0.0f;
+#pragma unroll
+            for (int j = 15; j >= 2; j--) {
+                // s_j = (L-j)/(j+1) r (1 + s_{j+1}); terms beyond L vanish
+                const float c = (float)(L - j) * (1.0f / (float)(j + 1));
+                s = (L - j > 0) ? c * r * (1.0f + s) : 0.0f;
             }
+            lu = logf(0.5f * (float)L * (float)(L - 1)) + 2.0f * lnx + (float)(L - 2) * log1pf(-x) + log1pf(s);
+        } else {
+            lu = logf(-expm1f((float)(L - 1) * log1pf(-x) + log1pf(y)));
         }
     }
-    if (u < 1e-300) u = 1e-300;  // S:333 floor
-    return log(u);
+    return fmaxf(lu, LOG_U_FLOOR);
 }
 
 // --------------------------------------------------------------------------

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         qv[g][3] = s_q[g][lane * 4 + 3];
     }
     const float4 cvec = reinterpret_cast<const float4*>(a.center + unit * HD)[lane];
-    const i128 r2q = a.mips ? ld_q64(a.r2 + unit * 2) : (i128)0;
+    const float* knorm = a.key_norm + unit * a.n_local;
     const uint16_t* kbase = a.k + unit * a.n_local * HD;
     const uint16_t* vbase = a.v + unit * a.n_local * HD;
     const int nsel = s_nsel;
@@ -291,20 +291,10 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
 #pragma unroll
         for (int g = 0; g < G; g++) lu[g] = 0.0f;
         if (inS) {
-            // the hashed key vector xbar_i (same arithmetic as the build)
+            // the hashed key vector xbar_i (same arithmetic as the build); |xbar_i| from the index
             const float x0 = bf2f(f2bf_rn(__fsub_rn(k0, cvec.x))), x1 = bf2f(f2bf_rn(__fsub_rn(k1, cvec.y)));
             const float x2 = bf2f(f2bf_rn(__fsub_rn(k2, cvec.z))), x3 = bf2f(f2bf_rn(__fsub_rn(k3, cvec.w)));
-            u128 n2 = q64_of_f32(__fmul_rn(x0, x0)) + q64_of_f32(__fmul_rn(x1, x1)) +
-                      q64_of_f32(__fmul_rn(x2, x2)) + q64_of_f32(__fmul_rn(x3, x3));
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) n2 += shfl_xor_u128(n2, m);
-            double xn2 = q64_to_double((i128)n2);
-            if (a.mips) {
-                i128 diff = r2q - (i128)n2;
-                float sv = diff > 0 ? bf2f(d2bf_rn_pos(sqrt(q64_to_double(diff)))) : 0.0f;
-                xn2 += (double)sv * (double)sv;
-            }
-            const float xnorm = (float)sqrt(xn2);
+            const float xnorm = __ldg(knorm + i);
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 if (inS & (1u << g)) {
@@ -312,8 +302,8 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                     float den = s_qn[g] * xnorm;
                     float cs = den > 0.0f ? dq / den : 0.0f;
                     cs = fminf(1.0f, fmaxf(-1.0f, cs));
-                    double p = 1.0 - (double)acosf(cs) * 0.31830988618379067;
-                    lu[g] = (float)log_sampling_prob(p, K, a.L, a.minc);
+                    const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
+                    lu[g] = log_sampling_prob(p, K, a.L, a.minc);
                 }
             }
         }

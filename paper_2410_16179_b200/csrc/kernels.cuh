@@ -20,8 +20,8 @@ int launch_key_norms(const uint16_t* k, int64_t units, int64_t n_local, int64_t 
 int launch_reduce_shards(int mode, const int64_t* parts_sum, const int64_t* parts_cnt, int P, int64_t units,
                          int64_t* out_sum, int64_t* out_cnt, cudaStream_t st);
 int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad, int mips, int KD,
-                const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, const float* W, int KL,
-                int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st);
+                const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, float* key_norm, const float* W,
+                int KL, int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st);
 int launch_hash_gemm(const uint8_t* xt, const uint8_t* wt, const float* xnorm, const float* wmax,
                      uint32_t* codes, uint2* fix_list, uint32_t* fix_count, uint32_t fix_cap, int64_t units,
                      int64_t n_local, int64_t n_pad, int64_t nchunks, int KD, int KL, int NT, int KLq,
@@ -35,13 +35,13 @@ struct DecodeArgs {
     const uint32_t* qbits;
     const uint32_t* codes;
     const float* center;
-    const int64_t* r2;
+    const float* key_norm;
     const uint16_t* k;
     const uint16_t* v;
     int64_t B, Hkv, Hq, n_local, seq_offset, n_global;
     int K, L, KL, KLw, KLq, ngroups, TG, QG;
     int64_t nchunks;
-    int tsplit, sink, local, minc, mips;
+    int tsplit, sink, local, minc;
     float* out;
     float* partial;
     int32_t* s_count;

@@ -11,18 +11,21 @@
 
 namespace mp {
 
-constexpr int QE_HEADS = 8;
+constexpr int QE_HEADS = 4;
 
 __global__ void __launch_bounds__(128) qencode_kernel(const uint16_t* __restrict__ q, int64_t BHq,
                                                       const float* __restrict__ W, int KL, int KLw,
                                                       uint32_t* __restrict__ qbits, uint32_t* status) {
-    __shared__ float qs[HD][QE_HEADS];
+    __shared__ double qd[HD][QE_HEADS];
+    __shared__ float qa[HD][QE_HEADS];
     const int tid = threadIdx.x;
     const int j = blockIdx.x * 128 + tid;
     const int64_t h0 = (int64_t)blockIdx.y * QE_HEADS;
     for (int e = tid; e < HD * QE_HEADS; e += 128) {
         int h = e / HD, d = e % HD;
-        qs[d][h] = (h0 + h < BHq) ? bf2f(q[(h0 + h) * HD + d]) : 0.0f;
+        float f = (h0 + h < BHq) ? bf2f(q[(h0 + h) * HD + d]) : 0.0f;
+        qd[d][h] = (double)f;
+        qa[d][h] = fabsf(f);
     }
     __syncthreads();
     double acc[QE_HEADS];
@@ -33,19 +36,23 @@ __global__ void __launch_bounds__(128) qencode_kernel(const uint16_t* __restrict
         bnd[h] = 0.0f;
     }
     const bool live = j < KL;
-#pragma unroll 4
+    const float* wp = W + (live ? j : 0);
+#pragma unroll 8
     for (int d = 0; d < HD; d++) {
-        float w = live ? __ldg(W + (int64_t)d * KL + j) : 0.0f;
-        float4 qa = *reinterpret_cast<const float4*>(&qs[d][0]);
-        float4 qb = *reinterpret_cast<const float4*>(&qs[d][4]);
-        const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        const float w = live ? __ldg(wp + (int64_t)d * KL) : 0.0f;
+        const double2 q01 = *reinterpret_cast<const double2*>(&qd[d][0]);
+        const double2 q23 = *reinterpret_cast<const double2*>(&qd[d][2]);
+        const float4 aq = *reinterpret_cast<const float4*>(&qa[d][0]);
         const double wd = (double)w;
         const float wa = fabsf(w);
-#pragma unroll
-        for (int h = 0; h < QE_HEADS; h++) {
-            acc[h] = fma((double)qv[h], wd, acc[h]);
-            bnd[h] = fmaf(fabsf(qv[h]), wa, bnd[h]);
-        }
+        acc[0] = fma(q01.x, wd, acc[0]);
+        acc[1] = fma(q01.y, wd, acc[1]);
+        acc[2] = fma(q23.x, wd, acc[2]);
+        acc[3] = fma(q23.y, wd, acc[3]);
+        bnd[0] = fmaf(aq.x, wa, bnd[0]);
+        bnd[1] = fmaf(aq.y, wa, bnd[1]);
+        bnd[2] = fmaf(aq.z, wa, bnd[2]);
+        bnd[3] = fmaf(aq.w, wa, bnd[3]);
     }
 #pragma unroll
     for (int h = 0; h < QE_HEADS; h++) {

@@ -26,6 +26,7 @@ class IndexBuffers:
     center: torch.Tensor   # [B][Hkv][128] f32
     r2: torch.Tensor       # [B][Hkv][2] int64 (q64)
     codes: torch.Tensor    # [codes_words] int32 (uint32 bit planes)
+    key_norm: torch.Tensor  # [B][Hkv][n] f32 |xbar_i|
     key_sum: torch.Tensor  # [B][Hkv][128][2] int64 (q64)
     count: torch.Tensor    # [B][Hkv] int64
 
@@ -57,6 +58,7 @@ class MagicPIG:
             center=torch.empty((Bn, Hkv, 128), dtype=torch.float32, device=dev),
             r2=torch.empty((Bn, Hkv, 2), dtype=torch.int64, device=dev),
             codes=torch.empty((max(words, 1),), dtype=torch.int32, device=dev),
+            key_norm=torch.empty((Bn, Hkv, max(n, 1)), dtype=torch.float32, device=dev),
             key_sum=torch.empty((Bn, Hkv, 128, 2), dtype=torch.int64, device=dev),
             count=torch.empty((Bn, Hkv), dtype=torch.int64, device=dev))
         nb = B_.build_workspace_bytes(self.cfg, Bn, Hkv, n)
@@ -78,7 +80,7 @@ class MagicPIG:
         Bn, Hkv, n, d = k.shape
         self._alloc(Bn, Hkv, n, k.device)
         b = self.buf
-        B_.build_index(self.cfg, k, self.W, b.center, b.r2, b.codes, b.key_sum, b.count, self._ws_build)
+        B_.build_index(self.cfg, k, self.W, b.center, b.r2, b.codes, b.key_norm, b.key_sum, b.count, self._ws_build)
         self.seq_offset, self.n_global, self.shape = 0, n, (Bn, Hkv, n)
         return self
 
@@ -103,7 +105,7 @@ class MagicPIG:
         all_r2 = torch.empty((P,) + tuple(r2_local.shape), dtype=r2_local.dtype, device=r2_local.device)
         dist.all_gather_into_tensor(all_r2, r2_local.contiguous(), group=group)
         B_.reduce_stats(1, all_r2, None, P, Bn, Hkv, b.r2, None)
-        B_.build_tables(self.cfg, k_local, seq_offset, n_global, self.W, b.center, b.r2, b.codes, ws)
+        B_.build_tables(self.cfg, k_local, seq_offset, n_global, self.W, b.center, b.r2, b.codes, b.key_norm, ws)
         self.seq_offset, self.n_global, self.shape = seq_offset, n_global, (Bn, Hkv, n)
         return self
 
@@ -117,7 +119,7 @@ class MagicPIG:
         if out is None and partial is None:
             out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=q.device)
         b = self.buf
-        B_.decode(self.cfg, q, b.codes, b.center, b.r2, k, v, self.seq_offset, self.n_global, self.W, ws,
+        B_.decode(self.cfg, q, b.codes, b.center, b.key_norm, k, v, self.seq_offset, self.n_global, self.W, ws,
                   out=out, partial=partial, s_count=s_count, s_mask=s_mask)
         return out if out is not None else partial
 

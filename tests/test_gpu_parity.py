@@ -205,7 +205,7 @@ def test_tensor_core_accumulation_error_bound():
     res = _run_gpu(wl, k, v, q, W, s_mask=False)
     mp = res["mp"]
     cfg = mp.cfg
-    nb = pkg.binding.build_workspace_bytes(cfg, 1, 1, 128) + 4 * pkg.binding.codes_words(cfg, 1, 1, 128) + 512
+    nb = pkg.binding.build_workspace_bytes(cfg, 1, 1, 128) + 4 * pkg.binding.codes_words(cfg, 1, 1, 128) + 1024
     ws = pkg.binding.new_workspace(nb, _dev())
     acc = torch.zeros((128, wl.K * wl.L), dtype=torch.float32, device=_dev())
     pkg.binding.debug_hash_acc(cfg, res["tk"][0, 0].contiguous(), res["tW"], mp.buf.center, mp.buf.r2, acc, ws)
@@ -256,10 +256,11 @@ def test_sequence_sharding_emulated():
     masks = []
     for p, (a, b, tk, tv, ws) in enumerate(shards):
         codes = torch.zeros((Bd.codes_words(cfg, 1, 2, b - a),), dtype=torch.int32, device=dev)
-        Bd.build_tables(cfg, tk, a, wl.n, tW, center, r2, codes, ws)
+        knorm = torch.zeros((1, 2, b - a), dtype=torch.float32, device=dev)
+        Bd.build_tables(cfg, tk, a, wl.n, tW, center, r2, codes, knorm, ws)
         wsd = Bd.new_workspace(Bd.decode_workspace_bytes(cfg, 1, 4, 2, b - a), dev)
         sm = torch.zeros((1, 4, (b - a + 31) // 32), dtype=torch.int32, device=dev)
-        Bd.decode(cfg, full["tq"], codes, center, r2, tk, tv, a, wl.n, tW, wsd, partial=parts[p], s_mask=sm)
+        Bd.decode(cfg, full["tq"], codes, center, knorm, tk, tv, a, wl.n, tW, wsd, partial=parts[p], s_mask=sm)
         masks.append((a, b, sm))
     out = torch.zeros((1, 4, 128), dtype=torch.float32, device=dev)
     Bd.merge_partials(parts, out)

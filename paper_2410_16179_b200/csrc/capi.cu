@@ -100,8 +100,6 @@ static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, in
 struct DecodeWs {
     uint32_t* status;
     uint32_t* qbits;
-    uint32_t* seen;
-    uint32_t* chunk_ctr;
     uint32_t* unit_ctr;
     float* parts;
     int32_t* chunk_cnt;
@@ -125,8 +123,6 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     };
     w.status = (uint32_t*)take(256);
     w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
-    w.seen = (uint32_t*)take((size_t)units * nch * G * 64 * 4);
-    w.chunk_ctr = (uint32_t*)take((size_t)units * nch * 4);
     w.unit_ctr = (uint32_t*)take((size_t)units * 4);
     w.parts = (float*)take((size_t)units * nch * G * PART * 4);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
@@ -291,13 +287,12 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
     a.TG = g.TG;
     a.QG = g.QG;
     a.nchunks = g.nchunks;
+    // cluster size: smallest power of two (<= 8) giving >= 1.5 CTAs per SM, with
+    // at least 8 table groups (one per warp) per CTA
     const int64_t total = B * Hkv * g.nchunks;
-    int64_t ts = (4 * (int64_t)num_sms() + total - 1) / total;
-    int64_t tsmax = g.ngroups / (DEC_THREADS / 32);
-    if (tsmax < 1) tsmax = 1;
-    if (ts > tsmax) ts = tsmax;
-    if (ts < 1) ts = 1;
-    a.tsplit = (int)ts;
+    int ts = 1;
+    while (ts < 8 && total * ts * 2 < 3 * (int64_t)num_sms() && g.ngroups / (2 * ts) >= DEC_THREADS / 32) ts *= 2;
+    a.tsplit = ts;
     a.sink = cfg->sink;
     a.local = cfg->local;
     a.minc = cfg->min_collisions;
@@ -305,8 +300,6 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
     a.partial = partial;
     a.s_count = s_count;
     a.s_mask = s_mask;
-    a.seen = w.seen;
-    a.chunk_ctr = w.chunk_ctr;
     a.unit_ctr = w.unit_ctr;
     a.parts = w.parts;
     a.chunk_cnt = w.chunk_cnt;

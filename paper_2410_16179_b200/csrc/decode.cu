@@ -1,27 +1,39 @@
 // decode.cu -- MagicPIG decode step (Algorithm 1).
 //
-// One CTA = one 1024-key chunk of one (sequence, kv head) unit, or a 1/tsplit
-// share of its tables when there are too few chunks to fill the GPU.
+// Grid: one thread-block CLUSTER of CS CTAs per 1024-key chunk of one
+// (sequence, kv head) unit; CTA r of the cluster scans table groups
+// [r*ng/CS, (r+1)*ng/CS).  8 warps per CTA; lane = 32-key block.
 //
-//  scan     Query(HT, q_code) over bit-plane codes: lane = 32-key block,
-//           128-bit coalesced loads; per table and query head one LOP3 per bit
-//           (m &= P_b ^ QX_b) and a saturating counter (seen1/seen2) gives the
-//           ">= 2 tables match" rule for 32 keys at once.
-//  combine  warps -> CTA via shared memory; CTAs of one chunk via atomicOr
-//           (exact: (a1,a2)+(b1,b2) = (a1|b1, a2|b2|(a1&b1))), last CTA goes on.
-//  compact  S_g (sampled, per query head) U T (sink/local) -> ascending
-//           list of chunk offsets (ballot/popc prefix sums).
-//  gather   warp per listed key: k, v rows (256 B each) -> logits q.k/sqrt(d)
-//           (P:109), for i in S_g: cos of the hashed vectors (R5), p, log u
-//           (fp64) and z = logit - log u; online softmax.
-//  merge    chunk partial (m, s, a) -> last CTA of the unit merges all chunks
-//           in fixed order (log-sum-exp, "recursive attention" P:171).
+//  stream   each warp streams its table groups (QG*512 contiguous bytes each)
+//           into a private shared-memory ring with cp.async.bulk + mbarrier;
+//           the first copies are issued BEFORE griddepcontrol.wait, so the
+//           code stream overlaps the query-encode kernel (PDL).
+//  scan     Query(HT, q_code): per table and query head one LOP3 per
+//           bit (m &= P_b ^ QX_b) and a saturating counter (seen1/seen2) gives
+//           the ">= 2 tables match" rule for 32 keys at once.
+//  combine  warps -> CTA via shared memory, CTAs -> cluster via DSMEM:
+//           (a1,a2)+(b1,b2) = (a1|b1, a2|b2|(a1&b1)); every CTA ends with the
+//           same S_g and the same ascending list of S U T (P:171 static keys).
+//  gather   CTA r takes list entries r, r+CS, ...; K/V rows (256 B each) and
+//           |xbar_i| staged by cp.async in double-buffered batches; warp per
+//           key: logits q.k/sqrt(d), cos of the hashed vectors (R5),
+//           p, log u (fp32, R11), z = logit - log u,
+//           online softmax.
+//  merge    CTA partials -> rank 0 via DSMEM -> chunk partial; the last chunk
+//           of a unit merges all chunks in fixed order (log-sum-exp,
+//           "recursive attention" P:171).  Counters self-clean (graph-safe).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cgr = cooperative_groups;
 
 namespace mp {
 
 constexpr int NWARP = DEC_THREADS / 32;
+constexpr int RB = 16;                   // rows per gather batch
+constexpr int ROWB = 2 * HD * 2 + 16;    // k row + v row + norm (padded) bytes
 constexpr float INV_SQRT_D = 0.08838834764831845f;  // 1/sqrt(128)
 
 // bits r of a 32-key block [base, base+32) whose local index lies in [lo, hi)
@@ -41,12 +53,16 @@ __device__ __forceinline__ float warp_sum_f(float v) {
     return v;
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <int G>
@@ -69,10 +85,37 @@ __device__ __forceinline__ void load_masks(const uint32_t* p, uint32_t (&q)[G]) 
     }
 }
 
+// online-softmax update of one head's running state with score z and value row
+__device__ __forceinline__ void osm_update(float z, float& m, float& s, float (&acc)[4], float v0, float v1,
+                                           float v2, float v3) {
+    if (z > m) {
+        const float sc = __expf(m - z);
+        s = s * sc + 1.0f;
+        acc[0] = acc[0] * sc + v0;
+        acc[1] = acc[1] * sc + v1;
+        acc[2] = acc[2] * sc + v2;
+        acc[3] = acc[3] * sc + v3;
+        m = z;
+    } else {
+        const float w = __expf(z - m);
+        s += w;
+        acc[0] += w * v0;
+        acc[1] += w * v1;
+        acc[2] += w * v2;
+        acc[3] += w * v3;
+    }
+}
+
 template <int K, int G>
 __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     constexpr int TG = tg_of(K), QG = qg_of(K);
-    extern __shared__ __align__(16) uint32_t qx[];  // [ncols][G] match masks
+    constexpr uint32_t GB = QG * 512;  // bytes of one table group of one chunk
+    extern __shared__ __align__(128) uint8_t dsm[];
+    uint32_t* qx = reinterpret_cast<uint32_t*>(dsm);           // [ncols][G] match masks
+    uint8_t* ring = dsm + a.qx_bytes;                           // [NWARP][depth][GB]
+    uint8_t* rows = ring + (size_t)NWARP * a.depth * GB;        // [2][RB][ROWB]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 2 * RB * ROWB);  // [NWARP][depth]
+
     __shared__ uint32_t s_part[NWARP][G][2][32];
     __shared__ uint32_t s_sel[G][32];
     __shared__ uint32_t s_tm[32];
@@ -83,45 +126,71 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __shared__ float s_a[NWARP][HD];
     __shared__ float s_q[G][HD];
     __shared__ float s_qn[G];
+    __shared__ float s_cm[G], s_cs[G];
+    __shared__ float s_ca[G][HD];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t cg = blockIdx.x / a.tsplit;  // global chunk = unit * nchunks + chunk
-    const int part = blockIdx.x % a.tsplit;
-    const int64_t unit = cg / a.nchunks, chunk = cg % a.nchunks;
+    const int CS = a.tsplit;
+    cgr::cluster_group cluster = cgr::this_cluster();
+    const int rank = CS > 1 ? (int)cluster.block_rank() : 0;
+    const int64_t cgid = blockIdx.x / CS;  // global chunk = unit * nchunks + chunk
+    const int64_t unit = cgid / a.nchunks, chunk = cgid % a.nchunks;
     const int64_t b = unit / a.Hkv, hkv = unit % a.Hkv;
     const int64_t qh0 = b * a.Hq + hkv * G;  // first query head (row of q) of this unit
-    const int g0 = (int)((int64_t)part * a.ngroups / a.tsplit);
-    const int g1 = (int)((int64_t)(part + 1) * a.ngroups / a.tsplit);
+    const int g0 = (int)((int64_t)rank * a.ngroups / CS);
+    const int g1 = (int)((int64_t)(rank + 1) * a.ngroups / CS);
     const int col0 = g0 * TG * K;
     const int ncols = (g1 - g0) * TG * K;
+    const int depth = a.depth;
 
-    // ---- query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
+    // ---- 1. start streaming this warp's code groups (independent of the query)
+    const uint8_t* csrc = reinterpret_cast<const uint8_t*>(a.codes) + (size_t)cgid * a.KLq * 512;
+    uint8_t* myring = ring + (size_t)warp * depth * GB;
+    uint64_t* mybar = bars + warp * depth;
+    const int n_my = g1 - g0 > warp ? (g1 - g0 - warp + NWARP - 1) / NWARP : 0;
+    if (lane == 0) {
+        for (int s = 0; s < depth; s++) mbar_init(mybar + s, 1);
+        fence_mbar_init();
+        for (int k = 0; k < depth && k < n_my; k++) {
+            const int grp = g0 + warp + k * NWARP;
+            mbar_arrive_expect_tx(mybar + k, GB);
+            bulk_g2s(myring + k * GB, csrc + (size_t)grp * GB, GB, mybar + k);
+        }
+    }
+    __syncwarp();
+
+    // ---- 2. wait for the query-encode kernel (programmatic dependent launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
     for (int e = tid; e < ncols * G; e += DEC_THREADS) {
-        int c = e / G, g = e % G;
-        int col = col0 + c;
+        const int c = e / G, g = e % G;
+        const int col = col0 + c;
         uint32_t bit = 0;
         if (col < a.KL) bit = (a.qbits[(qh0 + g) * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
         qx[e] = bit ? 0u : 0xffffffffu;
     }
+    for (int e = tid; e < G * HD; e += DEC_THREADS) s_q[e / HD][e % HD] = bf2f(a.q[(qh0 + e / HD) * HD + e % HD]);
     __syncthreads();
 
-    // ---- scan
+    // ---- 4. scan
     uint32_t s1[G], s2[G];
 #pragma unroll
     for (int g = 0; g < G; g++) s1[g] = s2[g] = 0u;
-    const uint4* cp = reinterpret_cast<const uint4*>(a.codes) + (cg * a.KLq) * 32 + lane;
-    int grp = g0 + warp;
-    uint4 P[QG];
-    if (grp < g1) {
+    for (int k = 0; k < n_my; k++) {
+        const int slot = k % depth;
+        const int grp = g0 + warp + k * NWARP;
+        mbar_wait(mybar + slot, (uint32_t)((k / depth) & 1));
+        uint4 P[QG];
+        const uint4* src = reinterpret_cast<const uint4*>(myring + slot * GB) + lane;
 #pragma unroll
-        for (int t = 0; t < QG; t++) P[t] = ldg_stream(cp + (int64_t)(grp * QG + t) * 32);
-    }
-    while (grp < g1) {
-        const int nxt = grp + NWARP;
-        uint4 Pn[QG];
-        if (nxt < g1) {
-#pragma unroll
-            for (int t = 0; t < QG; t++) Pn[t] = ldg_stream(cp + (int64_t)(nxt * QG + t) * 32);
+        for (int t = 0; t < QG; t++) P[t] = src[t * 32];
+        __syncwarp();
+        if (lane == 0 && k + depth < n_my) {
+            fence_proxy_async();
+            const int ng = grp + depth * NWARP;
+            mbar_arrive_expect_tx(mybar + slot, GB);
+            bulk_g2s(myring + slot * GB, csrc + (size_t)ng * GB, GB, mybar + slot);
         }
         const uint32_t* wv = reinterpret_cast<const uint32_t*>(P);
         const uint32_t* qrow = qx + (size_t)(grp - g0) * TG * K * G;
@@ -146,102 +215,91 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                 }
             }
         }
-#pragma unroll
-        for (int t = 0; t < QG; t++) P[t] = Pn[t];
-        grp = nxt;
     }
 
-    // ---- combine warps
+    // ---- 5. combine: warps -> CTA (shared), CTAs -> cluster (DSMEM)
 #pragma unroll
     for (int g = 0; g < G; g++) {
         s_part[warp][g][0][lane] = s1[g];
         s_part[warp][g][1][lane] = s2[g];
     }
     __syncthreads();
+    uint32_t f1 = 0, f2 = 0;  // valid in threads tid < G*32: (g = tid/32, block = lane)
     if (tid < G * 32) {
         const int g = tid >> 5;
-        uint32_t a1 = 0, a2 = 0;
         for (int w = 0; w < NWARP; w++) {
-            uint32_t b1 = s_part[w][g][0][lane], b2 = s_part[w][g][1][lane];
-            a2 |= b2 | (a1 & b1);
-            a1 |= b1;
+            const uint32_t b1 = s_part[w][g][0][lane], b2 = s_part[w][g][1][lane];
+            f2 |= b2 | (f1 & b1);
+            f1 |= b1;
         }
-        if (a.tsplit > 1) {
-            uint32_t* sg = a.seen + ((cg * G + g) * 2) * 32 + lane;
-            uint32_t old1 = atomicOr(sg, a1);
-            atomicOr(sg + 32, a2 | (old1 & a1));
-        }
-        s_part[0][g][0][lane] = a1;
-        s_part[0][g][1][lane] = a2;
-    }
-    if (a.tsplit > 1) {
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_flag = atomicAdd(a.chunk_ctr + cg, 1u) == (uint32_t)(a.tsplit - 1);
-        __syncthreads();
-        if (!s_flag) return;
-        __threadfence();
-        if (tid < G * 32) {
-            const int g = tid >> 5;
-            uint32_t* sg = a.seen + ((cg * G + g) * 2) * 32 + lane;
-            s_part[0][g][0][lane] = atomicExch(sg, 0u);
-            s_part[0][g][1][lane] = atomicExch(sg + 32, 0u);
-        }
-        if (tid == 0) a.chunk_ctr[cg] = 0u;
     }
     __syncthreads();
+    if (tid < G * 32) {
+        s_part[0][tid >> 5][0][lane] = f1;
+        s_part[0][tid >> 5][1][lane] = f2;
+    }
+    if (CS > 1) {
+        cluster.sync();
+        if (tid < G * 32) {
+            const int g = tid >> 5;
+            f1 = f2 = 0;
+            for (int r = 0; r < CS; r++) {
+                const uint32_t* rp = cluster.map_shared_rank(&s_part[0][g][0][0], r);
+                const uint32_t b1 = rp[lane], b2 = rp[32 + lane];
+                f2 |= b2 | (f1 & b1);
+                f1 |= b1;
+            }
+        }
+    }
 
-    // ---- final masks: S_g = count >= min_collisions, restricted to D; T = static keys
+    // ---- 6. final masks: S_g = count >= min_collisions restricted to D; T = static keys
     const int64_t cbase = chunk * KCHUNK;  // local index of the chunk's first key
     if (tid < 32) {
         const int64_t base = cbase + lane * 32;
-        uint32_t valid = range_mask(base, 0, a.n_local);
-        uint32_t tm = (range_mask(base, -a.seq_offset, (int64_t)a.sink - a.seq_offset) |
-                       range_mask(base, a.n_global - a.local - a.seq_offset, a.n_global - a.seq_offset)) &
-                      valid;
-        s_tm[lane] = tm;
+        const uint32_t valid = range_mask(base, 0, a.n_local);
+        s_tm[lane] = (range_mask(base, -a.seq_offset, (int64_t)a.sink - a.seq_offset) |
+                      range_mask(base, a.n_global - a.local - a.seq_offset, a.n_global - a.seq_offset)) &
+                     valid;
     }
     __syncthreads();
     if (tid < G * 32) {
         const int g = tid >> 5;
-        uint32_t v = (a.minc == 1 ? s_part[0][g][0][lane] : s_part[0][g][1][lane]);
+        uint32_t v = (a.minc == 1 ? f1 : f2);
         const int64_t base = cbase + lane * 32;
         v &= range_mask(base, 0, a.n_local) & ~s_tm[lane];
         s_sel[g][lane] = v;
-        int cnt = __popc(v);
+        if (rank == 0) {
+            int cnt = __popc(v);
 #pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
-        if (lane == 0) a.chunk_cnt[cg * G + g] = cnt;
-        if (a.s_mask) {
-            int64_t nw = (a.n_local + 31) >> 5;
-            int64_t widx = chunk * 32 + lane;
-            if (widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
+            for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
+            if (lane == 0) a.chunk_cnt[cgid * G + g] = cnt;
+            if (a.s_mask) {
+                const int64_t nw = (a.n_local + 31) >> 5;
+                const int64_t widx = chunk * 32 + lane;
+                if (widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
+            }
         }
-    }
-    // query vectors for the gather
-    for (int e = tid; e < G * HD; e += DEC_THREADS) s_q[e / HD][e % HD] = bf2f(a.q[(qh0 + e / HD) * HD + e % HD]);
-    __syncthreads();
-    if (tid < G * 32) {
-        const int g = tid >> 5;
-        float x0 = s_q[g][lane * 4], x1 = s_q[g][lane * 4 + 1], x2 = s_q[g][lane * 4 + 2], x3 = s_q[g][lane * 4 + 3];
-        float nn = warp_sum_f(x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3);
+        const float x0 = s_q[g][lane * 4], x1 = s_q[g][lane * 4 + 1], x2 = s_q[g][lane * 4 + 2],
+                    x3 = s_q[g][lane * 4 + 3];
+        const float nn = warp_sum_f(x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3);
         if (lane == 0) s_qn[g] = sqrtf(nn);
     }
-    // ---- compaction (ascending order) of U = (union_g S_g) U T
+    __syncthreads();
+    // ---- 7. compaction (ascending) of U = (union_g S_g) U T; identical in every CTA
     if (warp == 0) {
         uint32_t u = s_tm[lane];
 #pragma unroll
         for (int g = 0; g < G; g++) u |= s_sel[g][lane];
-        int c = __popc(u);
+        const int c = __popc(u);
         int incl = c;
 #pragma unroll
         for (int m = 1; m < 32; m <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, incl, m);
+            const int t = __shfl_up_sync(0xffffffffu, incl, m);
             if (lane >= m) incl += t;
         }
         int pos = incl - c;
         while (u) {
-            int r = __ffs(u) - 1;
+            const int r = __ffs(u) - 1;
             u &= u - 1;
             s_list[pos++] = (uint16_t)(lane * 32 + r);
         }
@@ -249,7 +307,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     }
     __syncthreads();
 
-    // ---- gather + estimator (warp per key, lane = 4 dims)
+    // ---- 8. gather + estimator: entries rank, rank+CS, ...; staged rows, warp per key
     float m_run[G], s_run[G], acc[G][4];
 #pragma unroll
     for (int g = 0; g < G; g++) {
@@ -270,68 +328,81 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     const uint16_t* kbase = a.k + unit * a.n_local * HD;
     const uint16_t* vbase = a.v + unit * a.n_local * HD;
     const int nsel = s_nsel;
-    for (int e = warp; e < nsel; e += NWARP) {
-        const int off = s_list[e];
-        const int64_t i = cbase + off;
-        const uint32_t bitm = 1u << (off & 31);
-        const bool is_t = (s_tm[off >> 5] & bitm) != 0;
-        uint32_t inS = 0;
+    const int n_mine = nsel > rank ? (nsel - rank + CS - 1) / CS : 0;
+    const int nbatch = (n_mine + RB - 1) / RB;
+
+    auto stage = [&](int bt) {  // issue cp.async for batch bt into buffer bt&1
+        uint8_t* buf = rows + (bt & 1) * RB * ROWB;
+        for (int e = tid; e < RB * 33; e += DEC_THREADS) {
+            const int rr = e / 33, part = e % 33;
+            const int j = bt * RB + rr;
+            if (j >= n_mine) continue;
+            const int64_t i = cbase + s_list[rank + j * CS];
+            uint8_t* dst = buf + rr * ROWB;
+            if (part < 16) cp_async16(dst + part * 16, kbase + i * HD + part * 8);
+            else if (part < 32) cp_async16(dst + 256 + (part - 16) * 16, vbase + i * HD + (part - 16) * 8);
+            else cp_async4(dst + 512, knorm + i);
+        }
+        cp_async_commit();
+    };
+    if (nbatch > 0) stage(0);
+    for (int bt = 0; bt < nbatch; bt++) {
+        if (bt + 1 < nbatch) {
+            stage(bt + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
+        for (int rr = warp; rr < RB; rr += NWARP) {
+            const int j = bt * RB + rr;
+            if (j >= n_mine) break;
+            const int off = s_list[rank + j * CS];
+            const uint32_t bitm = 1u << (off & 31);
+            const bool is_t = (s_tm[off >> 5] & bitm) != 0;
+            uint32_t inS = 0;
 #pragma unroll
-        for (int g = 0; g < G; g++) inS |= ((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g;
-        const uint2 kr = __ldg(reinterpret_cast<const uint2*>(kbase + i * HD) + lane);
-        const uint2 vr = __ldg(reinterpret_cast<const uint2*>(vbase + i * HD) + lane);
-        const float k0 = __uint_as_float(kr.x << 16), k1 = __uint_as_float(kr.x & 0xffff0000u);
-        const float k2 = __uint_as_float(kr.y << 16), k3 = __uint_as_float(kr.y & 0xffff0000u);
-        const float v0 = __uint_as_float(vr.x << 16), v1 = __uint_as_float(vr.x & 0xffff0000u);
-        const float v2 = __uint_as_float(vr.y << 16), v3 = __uint_as_float(vr.y & 0xffff0000u);
-        float logit[G];
+            for (int g = 0; g < G; g++) inS |= ((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g;
+            const uint8_t* row = buf + rr * ROWB;
+            const uint2 kr = *reinterpret_cast<const uint2*>(row + lane * 8);
+            const uint2 vr = *reinterpret_cast<const uint2*>(row + 256 + lane * 8);
+            const float k0 = __uint_as_float(kr.x << 16), k1 = __uint_as_float(kr.x & 0xffff0000u);
+            const float k2 = __uint_as_float(kr.y << 16), k3 = __uint_as_float(kr.y & 0xffff0000u);
+            const float v0 = __uint_as_float(vr.x << 16), v1 = __uint_as_float(vr.x & 0xffff0000u);
+            const float v2 = __uint_as_float(vr.y << 16), v3 = __uint_as_float(vr.y & 0xffff0000u);
+            float logit[G];
 #pragma unroll
-        for (int g = 0; g < G; g++) logit[g] = warp_sum_f(qv[g][0] * k0 + qv[g][1] * k1 + qv[g][2] * k2 + qv[g][3] * k3) * INV_SQRT_D;
-        float lu[G];
+            for (int g = 0; g < G; g++)
+                logit[g] = warp_sum_f(qv[g][0] * k0 + qv[g][1] * k1 + qv[g][2] * k2 + qv[g][3] * k3) * INV_SQRT_D;
+            float lu[G];
 #pragma unroll
-        for (int g = 0; g < G; g++) lu[g] = 0.0f;
-        if (inS) {
-            // the hashed key vector xbar_i (same arithmetic as the build); |xbar_i| from the index
-            const float x0 = bf2f(f2bf_rn(__fsub_rn(k0, cvec.x))), x1 = bf2f(f2bf_rn(__fsub_rn(k1, cvec.y)));
-            const float x2 = bf2f(f2bf_rn(__fsub_rn(k2, cvec.z))), x3 = bf2f(f2bf_rn(__fsub_rn(k3, cvec.w)));
-            const float xnorm = __ldg(knorm + i);
+            for (int g = 0; g < G; g++) lu[g] = 0.0f;
+            if (inS) {
+                // the hashed key vector xbar_i (same arithmetic as the build); |xbar_i| from the index
+                const float x0 = bf2f(f2bf_rn(__fsub_rn(k0, cvec.x))), x1 = bf2f(f2bf_rn(__fsub_rn(k1, cvec.y)));
+                const float x2 = bf2f(f2bf_rn(__fsub_rn(k2, cvec.z))), x3 = bf2f(f2bf_rn(__fsub_rn(k3, cvec.w)));
+                const float xnorm = *reinterpret_cast<const float*>(row + 512);
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                if (inS & (1u << g)) {
-                    float dq = warp_sum_f(qv[g][0] * x0 + qv[g][1] * x1 + qv[g][2] * x2 + qv[g][3] * x3);
-                    float den = s_qn[g] * xnorm;
-                    float cs = den > 0.0f ? dq / den : 0.0f;
-                    cs = fminf(1.0f, fmaxf(-1.0f, cs));
-                    const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
-                    lu[g] = log_sampling_prob(p, K, a.L, a.minc);
+                for (int g = 0; g < G; g++) {
+                    if (inS & (1u << g)) {
+                        const float dq = warp_sum_f(qv[g][0] * x0 + qv[g][1] * x1 + qv[g][2] * x2 + qv[g][3] * x3);
+                        const float den = s_qn[g] * xnorm;
+                        float cs = den > 0.0f ? dq / den : 0.0f;
+                        cs = fminf(1.0f, fmaxf(-1.0f, cs));
+                        const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
+                        lu[g] = log_sampling_prob(p, K, a.L, a.minc);
+                    }
                 }
             }
-        }
 #pragma unroll
-        for (int g = 0; g < G; g++) {
-            if (is_t || (inS & (1u << g))) {
-                const float z = logit[g] - lu[g];
-                if (z > m_run[g]) {
-                    const float sc = __expf(m_run[g] - z);
-                    s_run[g] = s_run[g] * sc + 1.0f;
-                    acc[g][0] = acc[g][0] * sc + v0;
-                    acc[g][1] = acc[g][1] * sc + v1;
-                    acc[g][2] = acc[g][2] * sc + v2;
-                    acc[g][3] = acc[g][3] * sc + v3;
-                    m_run[g] = z;
-                } else {
-                    const float w = __expf(z - m_run[g]);
-                    s_run[g] += w;
-                    acc[g][0] += w * v0;
-                    acc[g][1] += w * v1;
-                    acc[g][2] += w * v2;
-                    acc[g][3] += w * v3;
-                }
-            }
+            for (int g = 0; g < G; g++)
+                if (is_t || (inS & (1u << g))) osm_update(logit[g] - lu[g], m_run[g], s_run[g], acc[g], v0, v1, v2, v3);
         }
+        __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2)
     }
-    // ---- combine warp states -> chunk partial (one head at a time)
-    float* pc = a.parts + cg * G * PART;
+
+    // ---- 9. warps -> CTA partial per head
 #pragma unroll
     for (int g = 0; g < G; g++) {
         if (lane == 0) {
@@ -356,15 +427,43 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                     A += s_a[w][d] * f;
                 }
             }
+            s_ca[g][d] = A;
+            if (d == 0) {
+                s_cm[g] = M;
+                s_cs[g] = S;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- 10. cluster partials -> rank 0 -> chunk partial (global)
+    float* pc = a.parts + cgid * G * PART;
+    if (CS > 1) cluster.sync();
+    if (rank == 0) {
+        for (int e = tid; e < G * HD; e += DEC_THREADS) {
+            const int g = e / HD, d = e % HD;
+            float M = -INFINITY;
+            for (int r = 0; r < CS; r++) M = fmaxf(M, *cluster.map_shared_rank(&s_cm[g], r));
+            float S = 0.0f, A = 0.0f;
+            if (M != -INFINITY) {
+                for (int r = 0; r < CS; r++) {
+                    const float mr = *cluster.map_shared_rank(&s_cm[g], r);
+                    if (mr == -INFINITY) continue;
+                    const float f = __expf(mr - M);
+                    S += *cluster.map_shared_rank(&s_cs[g], r) * f;
+                    A += *cluster.map_shared_rank(&s_ca[g][d], r) * f;
+                }
+            }
             pc[g * PART + 2 + d] = A;
             if (d == 0) {
                 pc[g * PART] = M;
                 pc[g * PART + 1] = S;
             }
         }
-        __syncthreads();
     }
-    // ---- last chunk of the unit merges all chunks (fixed order)
+    if (CS > 1) cluster.sync();  // remote shared memory stays alive until rank 0 has read it
+    if (rank != 0) return;
+
+    // ---- 11. last chunk of the unit merges all chunks (fixed order)
     __threadfence();
     __syncthreads();
     if (tid == 0) s_flag = atomicAdd(a.unit_ctr + unit, 1u) == (uint32_t)(a.nchunks - 1);
@@ -437,17 +536,46 @@ int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
+size_t decode_dyn_smem(int K, int G, int ncols_max, int depth) {
+    size_t qxb = ((size_t)ncols_max * G * 4 + 127) & ~(size_t)127;
+    return qxb + (size_t)NWARP * depth * qg_of(K) * 512 + 2 * RB * ROWB + (size_t)NWARP * depth * 8;
+}
+
 template <int K, int G>
-static int launch_kg(const DecodeArgs& a, cudaStream_t st) {
+static int launch_kg(DecodeArgs a, cudaStream_t st) {
     constexpr int TG = tg_of(K);
-    int maxg = (a.ngroups + a.tsplit - 1) / a.tsplit + 1;
-    size_t smem = (size_t)maxg * TG * K * G * 4;
+    const int maxg = (a.ngroups + a.tsplit - 1) / a.tsplit;
+    const int ncols_max = maxg * TG * K;
+    a.qx_bytes = (int)(((size_t)ncols_max * G * 4 + 127) & ~(size_t)127);
+    a.depth = 3;
+    if (decode_dyn_smem(K, G, ncols_max, 3) > 100 * 1024) a.depth = 2;
+    size_t smem = decode_dyn_smem(K, G, ncols_max, a.depth);
     auto kern = decode_kernel<K, G>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int64_t nblk = a.B * a.Hkv * a.nchunks * a.tsplit;
-    kern<<<(unsigned)nblk, DEC_THREADS, smem, st>>>(a);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return MAGICPIG_ECUDA;
+    const int64_t nblk = a.B * a.Hkv * a.nchunks * a.tsplit;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nblk);
+    cfg.blockDim = dim3(DEC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[2];
+    int na = 0;
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+    if (a.tsplit > 1) {
+        attrs[na].id = cudaLaunchAttributeClusterDimension;
+        attrs[na].val.clusterDim.x = (unsigned)a.tsplit;
+        attrs[na].val.clusterDim.y = 1;
+        attrs[na].val.clusterDim.z = 1;
+        na++;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     count_launch(1);
-    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+    return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
 template <int K>

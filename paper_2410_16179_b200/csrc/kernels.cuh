@@ -42,12 +42,11 @@ struct DecodeArgs {
     int K, L, KL, KLw, KLq, ngroups, TG, QG;
     int64_t nchunks;
     int tsplit, sink, local, minc;
+    int qx_bytes, depth;  // set by the launcher
     float* out;
     float* partial;
     int32_t* s_count;
     uint32_t* s_mask;
-    uint32_t* seen;
-    uint32_t* chunk_ctr;
     uint32_t* unit_ctr;
     float* parts;
     int32_t* chunk_cnt;

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     uint8_t* ring = dsm + a.qx_bytes;                           // [NWARP][depth][GB]
     uint8_t* rows = ring + (size_t)NWARP * a.depth * GB;        // [2][RB][ROWB]
     uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 2 * RB * ROWB);  // [NWARP][depth]
+    uint32_t* qb = reinterpret_cast<uint32_t*>(bars + NWARP * a.depth);  // [G][KLw] packed query bits
 
     __shared__ uint32_t s_part[NWARP][G][2][32];
     __shared__ uint32_t s_sel[G][32];
@@ -163,14 +164,16 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
+    for (int e = tid; e < G * a.KLw; e += DEC_THREADS) qb[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
+    for (int e = tid; e < G * HD; e += DEC_THREADS) s_q[e / HD][e % HD] = bf2f(a.q[(qh0 + e / HD) * HD + e % HD]);
+    __syncthreads();
     for (int e = tid; e < ncols * G; e += DEC_THREADS) {
         const int c = e / G, g = e % G;
         const int col = col0 + c;
         uint32_t bit = 0;
-        if (col < a.KL) bit = (a.qbits[(qh0 + g) * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
+        if (col < a.KL) bit = (qb[g * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
         qx[e] = bit ? 0u : 0xffffffffu;
     }
-    for (int e = tid; e < G * HD; e += DEC_THREADS) s_q[e / HD][e % HD] = bf2f(a.q[(qh0 + e / HD) * HD + e % HD]);
     __syncthreads();
 
     // ---- 4. scan
@@ -471,19 +474,47 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     if (!s_flag) return;
     __threadfence();
     const float* pu = a.parts + unit * a.nchunks * G * PART;
+    const int nch = (int)a.nchunks;
+    float* f = reinterpret_cast<float*>(rows);  // reuse the row buffers: [nch][G] scale factors
+    // (a) M_g = max_c m_c,g : warp g, lanes stride over chunks
+    if (warp < G) {
+        float M = -INFINITY;
+        for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(pu + ((int64_t)c * G + warp) * PART));
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, m));
+        if (lane == 0) s_cm[warp] = M;
+    }
+    __syncthreads();
+    // (b) f_c,g = e^{m_c,g - M_g};  S_g = sum_c f_c,g s_c,g
+    const bool fit = nch * G * 4 <= 2 * RB * ROWB;
+    if (warp < G) {
+        const float M = s_cm[warp];
+        float S = 0.0f;
+        for (int c = lane; c < nch; c += 32) {
+            const float mc = __ldcg(pu + ((int64_t)c * G + warp) * PART);
+            const float fc = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
+            if (fit) f[c * G + warp] = fc;
+            S += fc * __ldcg(pu + ((int64_t)c * G + warp) * PART + 1);
+        }
+        S = warp_sum_f(S);
+        if (lane == 0) s_cs[warp] = S;
+    }
+    __syncthreads();
+    // (c) A_g,d = sum_c f_c,g a_c,g,d  (fixed chunk order)
     for (int e = tid; e < G * HD; e += DEC_THREADS) {
         const int g = e / HD, d = e % HD;
-        float M = -INFINITY;
-        for (int64_t c = 0; c < a.nchunks; c++) M = fmaxf(M, __ldcg(pu + (c * G + g) * PART));
-        float S = 0.0f, A = 0.0f;
-        if (M != -INFINITY) {
-            for (int64_t c = 0; c < a.nchunks; c++) {
-                const float mc = __ldcg(pu + (c * G + g) * PART);
-                if (mc == -INFINITY) continue;
-                const float f = __expf(mc - M);
-                S += __ldcg(pu + (c * G + g) * PART + 1) * f;
-                A += __ldcg(pu + (c * G + g) * PART + 2 + d) * f;
+        const float M = s_cm[g], S = s_cs[g];
+        float A = 0.0f;
+#pragma unroll 8
+        for (int c = 0; c < nch; c++) {
+            float fc;
+            if (fit) {
+                fc = f[c * G + g];
+            } else {
+                const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
+                fc = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
             }
+            A += fc * __ldcg(pu + ((int64_t)c * G + g) * PART + 2 + d);
         }
         const int64_t row = qh0 + g;
         if (a.out) a.out[row * HD + d] = S > 0.0f ? A / S : 0.0f;
@@ -498,7 +529,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
             if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
             if (a.s_count) {
                 int tot = 0;
-                for (int64_t c = 0; c < a.nchunks; c++) tot += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + g);
+                for (int c = 0; c < nch; c++) tot += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + g);
                 a.s_count[row] = tot;
             }
         }
@@ -536,9 +567,10 @@ int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
-size_t decode_dyn_smem(int K, int G, int ncols_max, int depth) {
+size_t decode_dyn_smem(int K, int G, int ncols_max, int depth, int KLw) {
     size_t qxb = ((size_t)ncols_max * G * 4 + 127) & ~(size_t)127;
-    return qxb + (size_t)NWARP * depth * qg_of(K) * 512 + 2 * RB * ROWB + (size_t)NWARP * depth * 8;
+    return qxb + (size_t)NWARP * depth * qg_of(K) * 512 + 2 * RB * ROWB + (size_t)NWARP * depth * 8 +
+           (size_t)G * KLw * 4;
 }
 
 template <int K, int G>
@@ -548,8 +580,8 @@ static int launch_kg(DecodeArgs a, cudaStream_t st) {
     const int ncols_max = maxg * TG * K;
     a.qx_bytes = (int)(((size_t)ncols_max * G * 4 + 127) & ~(size_t)127);
     a.depth = 3;
-    if (decode_dyn_smem(K, G, ncols_max, 3) > 100 * 1024) a.depth = 2;
-    size_t smem = decode_dyn_smem(K, G, ncols_max, a.depth);
+    if (decode_dyn_smem(K, G, ncols_max, 3, a.KLw) > 100 * 1024) a.depth = 2;
+    size_t smem = decode_dyn_smem(K, G, ncols_max, a.depth, a.KLw);
     auto kern = decode_kernel<K, G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MAGICPIG_ECUDA;

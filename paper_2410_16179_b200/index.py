@@ -19,6 +19,7 @@ from typing import Optional
 import torch
 
 from . import binding as B_
+from .sharding import all_gather_stacked
 
 
 @dataclass
@@ -95,15 +96,12 @@ class MagicPIG:
         ks = torch.empty_like(b.key_sum)
         cnt = torch.empty_like(b.count)
         B_.key_stats(self.cfg, k_local, seq_offset, n_global, ks, cnt, ws)
-        all_ks = torch.empty((P,) + tuple(ks.shape), dtype=ks.dtype, device=ks.device)
-        all_cnt = torch.empty((P,) + tuple(cnt.shape), dtype=cnt.dtype, device=cnt.device)
-        dist.all_gather_into_tensor(all_ks, ks.contiguous(), group=group)
-        dist.all_gather_into_tensor(all_cnt, cnt.contiguous(), group=group)
+        all_ks = all_gather_stacked(ks, group)
+        all_cnt = all_gather_stacked(cnt, group)
         B_.reduce_stats(0, all_ks, all_cnt, P, Bn, Hkv, b.key_sum, b.count)
         r2_local = torch.empty_like(b.r2)
         B_.key_norms(self.cfg, k_local, seq_offset, n_global, b.key_sum, b.count, b.center, r2_local, ws)
-        all_r2 = torch.empty((P,) + tuple(r2_local.shape), dtype=r2_local.dtype, device=r2_local.device)
-        dist.all_gather_into_tensor(all_r2, r2_local.contiguous(), group=group)
+        all_r2 = all_gather_stacked(r2_local, group)
         B_.reduce_stats(1, all_r2, None, P, Bn, Hkv, b.r2, None)
         B_.build_tables(self.cfg, k_local, seq_offset, n_global, self.W, b.center, b.r2, b.codes, b.key_norm, ws)
         self.seq_offset, self.n_global, self.shape = seq_offset, n_global, (Bn, Hkv, n)
@@ -125,14 +123,11 @@ class MagicPIG:
 
     def decode_sharded(self, q, k_local, v_local, group=None, out=None, s_count=None):
         """Sequence-sharded decode: partial states, one all-gather, fixed-order merge."""
-        import torch.distributed as dist
         Bn, Hkv, n, _ = k_local.shape
         Hq = q.shape[1]
-        P = dist.get_world_size(group)
         part = torch.empty((Bn * Hq, B_.PART), dtype=torch.float32, device=q.device)
         self.decode(q, k_local, v_local, partial=part, s_count=s_count)
-        allp = torch.empty((P, Bn * Hq, B_.PART), dtype=torch.float32, device=q.device)
-        dist.all_gather_into_tensor(allp, part, group=group)
+        allp = all_gather_stacked(part, group)
         if out is None:
             out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=q.device)
         B_.merge_partials(allp, out)

@@ -290,3 +290,34 @@ def test_c2_full_size_sampled_unit():
     ref = oracle.decode_unit(k[0, h], v[0, h], q[0, h * wl.G:(h + 1) * wl.G], W, wl.K, wl.L, wl.center, wl.mips,
                              wl.min_collisions, wl.sink, wl.local)
     _check_unit(wl, res, ref, 0, h, wl.n)
+
+
+def test_query_codes_near_zero_dots():
+    """Query-code signs where the fp32 certificate fails: exact zeros (sign(0)=0,
+    R6) and dots cancelling to ~2^-20 of their terms go through the fp64 and
+    exact-integer fallbacks; every bit must equal the oracle's."""
+    pkg = _pkg()
+    rng = np.random.default_rng(77)
+    K, L = 4, 40
+    KL = K * L
+    bf = synth.bf16_bits_from_f32
+    q = synth.bf16_bits_to_f32(bf(rng.standard_normal((1, 3, 128), dtype=np.float32)))
+    W = synth.bf16_bits_to_f32(bf(rng.standard_normal((128, KL), dtype=np.float32)))
+    q[0, 0, :] = 0.0
+    q[0, 0, 0], q[0, 0, 1], q[0, 0, 2] = 1.0, -1.0, 2.0 ** -20
+    for j in range(0, KL, 3):  # columns with an exact zero or a tiny dot against head 0
+        W[:, j] = 0.0
+        W[0, j] = W[1, j] = np.float32(rng.choice([0.5, 1.0, 3.0]))
+        W[2, j] = np.float32(rng.choice([0.0, 1.0, -1.0]))
+    q[0, 1] = q[0, 0] * -1
+    cfg = pkg.binding.make_config(K=K, L=L, mips=0)
+    tq = _bf(bf(q))
+    tW = torch.from_numpy(np.ascontiguousarray(W)).to(_dev())
+    qc = torch.zeros((1, 3, L), dtype=torch.int16, device=_dev())
+    ws = pkg.binding.new_workspace(pkg.binding.decode_workspace_bytes(cfg, 1, 3, 1, 0) + 4096, _dev())
+    pkg.binding.query_codes(cfg, tq, tW, qc, ws)
+    torch.cuda.synchronize()
+    got = qc.cpu().numpy().view(np.uint16)
+    assert pkg.binding.workspace_status(ws) == 0
+    for h in range(3):
+        np.testing.assert_array_equal(got[0, h], oracle.encode_query(bf(q[0, h]), W, K, L, 0))

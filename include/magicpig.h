@@ -206,6 +206,19 @@ int magicpig_debug_hash_acc(const magicpig_config* cfg, const uint16_t* k, int64
                             const float* W, const float* center, const int64_t* r2, float* acc,
                             void* ws, size_t ws_bytes, void* stream);
 
+/* Debug timeline of one decode (encode + decode_encoded, unsharded): thread 0
+ * of every decode CTA writes %globaltimer (ns) at its phase boundaries into
+ * timeline[cta][16] (0 = not reached): 0 start, 1 after griddepcontrol.wait,
+ * 2 query masks, 3 scan, 4 cluster combine, 5 compaction, 6 gather,
+ * 7 CTA partial, 8 cluster merge, 9 unit-merge start, 10 end.  Returns the
+ * number of CTAs (> 0) or an error code. */
+int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                       const uint32_t* codes, const float* center, const float* key_norm,
+                                       const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
+                                       int64_t n_local, const float* W, float* out,
+                                       unsigned long long* timeline, int64_t timeline_len, void* ws,
+                                       size_t ws_bytes, void* stream);
+
 /* Message for an error code. [host] */
 const char* magicpig_strerror(int err);
 

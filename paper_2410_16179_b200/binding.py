@@ -59,6 +59,8 @@ _SIGS = {
     "magicpig_query_codes": ([_p, _p, _i64, _i64, _p, _p, _p, _sz, _p], _i),
     "magicpig_collision_counts": ([_p, _p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_hash_acc": ([_p, _p, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
+    "magicpig_debug_decode_timeline": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _p,
+                                        _sz, _p], _i64),
     "magicpig_strerror": ([_i], C.c_char_p),
     "magicpig_version": ([], C.c_char_p),
     "magicpig_launch_count": ([], C.c_uint64),
@@ -236,6 +238,17 @@ def debug_hash_acc(cfg, k_unit, W, center, r2, acc, ws):
     n = k_unit.shape[0]
     _check(lib().magicpig_debug_hash_acc(_cfg(cfg), _ptr(k_unit), n, _ptr(W), _ptr(center), _ptr(r2), _ptr(acc),
                                          _ptr(ws), ws.numel(), _stream()), "debug_hash_acc")
+
+
+def debug_decode_timeline(cfg, q, codes, center, key_norm, k, v, W, out, timeline, ws) -> int:
+    Bn, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    rc = lib().magicpig_debug_decode_timeline(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(key_norm),
+                                              _ptr(k), _ptr(v), Bn, Hkv, n, _ptr(W), _ptr(out), _ptr(timeline),
+                                              timeline.numel(), _ptr(ws), ws.numel(), _stream())
+    if rc < 0:
+        _check(int(rc), "debug_decode_timeline")
+    return int(rc)
 
 
 def launch_count() -> int:

@@ -237,11 +237,11 @@ int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64
     return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
 }
 
-int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
-                            const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B,
-                            int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
-                            float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
-                            void* stream) {
+static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
+                       const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B,
+                       int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
+                       float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
+                       void* stream, unsigned long long* timeline, int64_t timeline_len, int64_t* grid_out) {
     if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
     if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
     const int64_t G = Hq / Hkv;
@@ -304,7 +304,38 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
     a.parts = w.parts;
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
+    const int64_t grid = B * Hkv * g.nchunks * a.tsplit;
+    if (grid_out) *grid_out = grid;
+    if (timeline) {
+        if (timeline_len < grid * 16) return MAGICPIG_EINVAL;
+        if (cudaMemsetAsync(timeline, 0, (size_t)grid * 16 * 8, st) != cudaSuccess) return MAGICPIG_ECUDA;
+        a.timeline = timeline;
+    }
     return launch_decode(a, st);
+}
+
+extern "C" int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                       const uint32_t* codes, const float* center, const float* key_norm,
+                                       const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local,
+                                       int64_t seq_offset, int64_t n_global, float* out, float* partial,
+                                       int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes, void* stream) {
+    return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
+                       partial, s_count, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr);
+}
+
+extern "C" int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                                  const uint32_t* codes, const float* center, const float* key_norm,
+                                                  const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
+                                                  int64_t n_local, const float* W, float* out,
+                                                  unsigned long long* timeline, int64_t timeline_len, void* ws,
+                                                  size_t ws_bytes, void* stream) {
+    if (!timeline) return MAGICPIG_EINVAL;
+    int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
+    if (rc) return rc;
+    int64_t grid = 0;
+    rc = decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, 0, n_local, out, nullptr, nullptr,
+                     nullptr, ws, ws_bytes, stream, timeline, timeline_len, &grid);
+    return rc ? rc : grid;
 }
 
 int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,

@@ -106,6 +106,16 @@ __device__ __forceinline__ void osm_update(float z, float& m, float& s, float (&
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define MP_STAMP(ph)                                                                        \
+    do {                                                                                     \
+        if (a.timeline && threadIdx.x == 0) a.timeline[(size_t)blockIdx.x * 16 + (ph)] = gtimer(); \
+    } while (0)
+
 template <int K, int G>
 __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     constexpr int TG = tg_of(K), QG = qg_of(K);
@@ -143,6 +153,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     const int col0 = g0 * TG * K;
     const int ncols = (g1 - g0) * TG * K;
     const int depth = a.depth;
+    MP_STAMP(0);
 
     // ---- 1. start streaming this warp's code groups (independent of the query)
     const uint8_t* csrc = reinterpret_cast<const uint8_t*>(a.codes) + (size_t)cgid * a.KLq * 512;
@@ -162,6 +173,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
 
     // ---- 2. wait for the query-encode kernel (programmatic dependent launch)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    MP_STAMP(1);
 
     // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
     for (int e = tid; e < G * a.KLw; e += DEC_THREADS) qb[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
@@ -175,6 +187,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         qx[e] = bit ? 0u : 0xffffffffu;
     }
     __syncthreads();
+    MP_STAMP(2);
 
     // ---- 4. scan
     uint32_t s1[G], s2[G];
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         s_part[warp][g][1][lane] = s2[g];
     }
     __syncthreads();
+    MP_STAMP(3);
     uint32_t f1 = 0, f2 = 0;  // valid in threads tid < G*32: (g = tid/32, block = lane)
     if (tid < G * 32) {
         const int g = tid >> 5;
@@ -255,6 +269,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
     }
 
+    MP_STAMP(4);
     // ---- 6. final masks: S_g = count >= min_collisions restricted to D; T = static keys
     const int64_t cbase = chunk * KCHUNK;  // local index of the chunk's first key
     if (tid < 32) {
@@ -310,6 +325,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     }
     __syncthreads();
 
+    MP_STAMP(5);
     // ---- 8. gather + estimator: entries rank, rank+CS, ...; staged rows, warp per key
     float m_run[G], s_run[G], acc[G][4];
 #pragma unroll
@@ -405,6 +421,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2)
     }
 
+    MP_STAMP(6);
     // ---- 9. warps -> CTA partial per head
 #pragma unroll
     for (int g = 0; g < G; g++) {
@@ -438,6 +455,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
         __syncthreads();
     }
+    MP_STAMP(7);
     // ---- 10. cluster partials -> rank 0 -> chunk partial (global)
     float* pc = a.parts + cgid * G * PART;
     if (CS > 1) cluster.sync();
@@ -464,6 +482,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
     }
     if (CS > 1) cluster.sync();  // remote shared memory stays alive until rank 0 has read it
+    MP_STAMP(8);
     if (rank != 0) return;
 
     // ---- 11. last chunk of the unit merges all chunks (fixed order)
@@ -473,6 +492,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __syncthreads();
     if (!s_flag) return;
     __threadfence();
+    MP_STAMP(9);
     const float* pu = a.parts + unit * a.nchunks * G * PART;
     const int nch = (int)a.nchunks;
     float* f = reinterpret_cast<float*>(rows);  // reuse the row buffers: [nch][G] scale factors
@@ -535,6 +555,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
     }
     if (tid == 0) a.unit_ctr[unit] = 0u;
+    MP_STAMP(10);
 }
 
 // P-way merge of partial states (sequence shards): parts [P][BH][130]

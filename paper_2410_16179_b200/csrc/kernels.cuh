@@ -43,6 +43,7 @@ struct DecodeArgs {
     int64_t nchunks;
     int tsplit, sink, local, minc;
     int qx_bytes, depth;  // set by the launcher
+    unsigned long long* timeline;  // debug: [grid][16] globaltimer stamps, or NULL
     float* out;
     float* partial;
     int32_t* s_count;

@@ -30,15 +30,32 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j0 = blockIdx.x * QE_COLS;
     const int64_t h0 = (int64_t)blockIdx.y * QE_HPB;
-    for (int e = tid; e < HD * QE_COLS; e += QE_THREADS) {
-        const int d = e / QE_COLS, c = e % QE_COLS;
-        ws[d][c] = (j0 + c < KL) ? __ldg(W + (int64_t)d * KL + j0 + c) : 0.0f;
-    }
-    for (int e = tid; e < HD * QE_HPB; e += QE_THREADS) {
-        const int h = e / HD, d = e % HD;
-        const float f = (h0 + h < BHq) ? bf2f(q[(h0 + h) * HD + d]) : 0.0f;
-        qs[d][h] = f;
-        qa[d][h] = fabsf(f);
+    {   // all loads in flight before any store (16 W values + 8 q values per thread)
+        constexpr int NW = HD * QE_COLS / QE_THREADS, NQ = HD * QE_HPB / QE_THREADS;
+        float wv[NW];
+        uint16_t qv[NQ];
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            const int e = tid + i * QE_THREADS, d = e / QE_COLS, c = e % QE_COLS;
+            wv[i] = (j0 + c < KL) ? __ldg(W + (int64_t)d * KL + j0 + c) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < NQ; i++) {
+            const int e = tid + i * QE_THREADS, h = e / HD, d = e % HD;
+            qv[i] = (h0 + h < BHq) ? __ldg(q + (h0 + h) * HD + d) : (uint16_t)0;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            const int e = tid + i * QE_THREADS;
+            ws[e / QE_COLS][e % QE_COLS] = wv[i];
+        }
+#pragma unroll
+        for (int i = 0; i < NQ; i++) {
+            const int e = tid + i * QE_THREADS, h = e / HD, d = e % HD;
+            const float f = bf2f(qv[i]);
+            qs[d][h] = f;
+            qa[d][h] = fabsf(f);
+        }
     }
     __syncthreads();
     const int hs = warp & 3, dh = warp >> 2;

@@ -124,7 +124,7 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     w.status = (uint32_t*)take(256);
     w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
     w.unit_ctr = (uint32_t*)take((size_t)units * 4);
-    w.parts = (float*)take((size_t)units * nch * G * PART * 4);
+    w.parts = (float*)take((size_t)units * nch * 8 * G * PART * 4);  // up to 8 CTAs (cluster) per chunk
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
     w.bytes = off;
     return w;

@@ -32,7 +32,9 @@ namespace cgr = cooperative_groups;
 namespace mp {
 
 constexpr int NWARP = DEC_THREADS / 32;
-constexpr int RB = 16;                   // rows per gather batch
+constexpr int RB = 32;                   // rows (keys) per gather batch
+constexpr int XS = 272;                  // bytes per row of the bf16 xbar tile (16-B aligned, conflict-free ldmatrix)
+constexpr int QBS = 272;                 // bytes per row of the bf16 query tile
 constexpr int ROWB = 2 * HD * 2 + 16;    // k row + v row + norm (padded) bytes
 constexpr float INV_SQRT_D = 0.08838834764831845f;  // 1/sqrt(128)
 
@@ -116,15 +118,34 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (a.timeline && threadIdx.x == 0) a.timeline[(size_t)blockIdx.x * 16 + (ph)] = gtimer(); \
     } while (0)
 
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D, fp32 accumulate (exact products)
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 template <int K, int G>
 __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     constexpr int TG = tg_of(K), QG = qg_of(K);
     constexpr uint32_t GB = QG * 512;  // bytes of one table group of one chunk
+    constexpr int NITEM = (G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS;  // (head, dim pair) items per thread
     extern __shared__ __align__(128) uint8_t dsm[];
-    uint32_t* qx = reinterpret_cast<uint32_t*>(dsm);           // [ncols][G] match masks
-    uint8_t* ring = dsm + a.qx_bytes;                           // [NWARP][depth][GB]
-    uint8_t* rows = ring + (size_t)NWARP * a.depth * GB;        // [2][RB][ROWB]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rows + 2 * RB * ROWB);  // [NWARP][depth]
+    uint32_t* qx = reinterpret_cast<uint32_t*>(dsm);  // [ncols][G] match masks
+    uint8_t* ring = dsm + a.qx_bytes;                  // scan: [NWARP][depth][GB]; gather: rows + x tile
+    uint8_t* rows = ring;                              // [2][RB][ROWB]
+    uint8_t* xt = ring + 2 * RB * ROWB;                // [RB][XS] bf16 xbar rows
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + a.ring_bytes);  // [NWARP][depth]
     uint32_t* qb = reinterpret_cast<uint32_t*>(bars + NWARP * a.depth);  // [G][KLw] packed query bits
 
     __shared__ uint32_t s_part[NWARP][G][2][32];
@@ -133,12 +154,13 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __shared__ uint16_t s_list[KCHUNK];
     __shared__ int s_nsel;
     __shared__ uint32_t s_flag;
-    __shared__ float s_m[NWARP][G], s_s[NWARP][G];
-    __shared__ float s_a[NWARP][HD];
-    __shared__ float s_q[G][HD];
+    __shared__ __align__(16) uint8_t s_qb16[8 * QBS];  // query heads as bf16 rows (B operand), zero padded
+    __shared__ float s_c[HD];
     __shared__ float s_qn[G];
-    __shared__ float s_cm[G], s_cs[G];
-    __shared__ float s_ca[G][HD];
+    __shared__ float s_zl[RB][8], s_zd[RB][8], s_w[RB][8];
+    __shared__ float s_mrun[G], s_srun[G], s_scale[G];
+    __shared__ float s_xn[RB];
+    __shared__ uint8_t s_sel_k[RB];  // bit g: key in S_g; bit 7: static
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int CS = a.tsplit;
@@ -169,6 +191,14 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
             bulk_g2s(myring + k * GB, csrc + (size_t)grp * GB, GB, mybar + k);
         }
     }
+    // query rows (bf16 B operand, heads >= G zero) and centering vector: no dependency on the encode
+    for (int e = tid; e < 8 * (HD / 2); e += DEC_THREADS) {
+        const int g = e / (HD / 2), dp = e % (HD / 2);
+        uint32_t v = 0;
+        if (g < G) v = __ldg(reinterpret_cast<const uint32_t*>(a.q + (qh0 + g) * HD) + dp);
+        *reinterpret_cast<uint32_t*>(s_qb16 + g * QBS + dp * 4) = v;
+    }
+    if (tid < HD) s_c[tid] = __ldg(a.center + unit * HD + tid);
     __syncwarp();
 
     // ---- 2. wait for the query-encode kernel (programmatic dependent launch)
@@ -177,7 +207,6 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
 
     // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
     for (int e = tid; e < G * a.KLw; e += DEC_THREADS) qb[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
-    for (int e = tid; e < G * HD; e += DEC_THREADS) s_q[e / HD][e % HD] = bf2f(a.q[(qh0 + e / HD) * HD + e % HD]);
     __syncthreads();
     for (int e = tid; e < ncols * G; e += DEC_THREADS) {
         const int c = e / G, g = e % G;
@@ -185,6 +214,14 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         uint32_t bit = 0;
         if (col < a.KL) bit = (qb[g * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
         qx[e] = bit ? 0u : 0xffffffffu;
+    }
+    if (tid < G * 32) {  // |q_g|
+        const int g = tid >> 5;
+        const uint2 qq = *reinterpret_cast<const uint2*>(s_qb16 + g * QBS + lane * 8);
+        const float x0 = __uint_as_float(qq.x << 16), x1 = __uint_as_float(qq.x & 0xffff0000u);
+        const float x2 = __uint_as_float(qq.y << 16), x3 = __uint_as_float(qq.y & 0xffff0000u);
+        const float nn = warp_sum_f(x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3);
+        if (lane == 0) s_qn[g] = sqrtf(nn);
     }
     __syncthreads();
     MP_STAMP(2);
@@ -267,9 +304,11 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                 f1 |= b1;
             }
         }
+        // remote reads done: let the peers go on; we wait for them only before exiting
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     }
-
     MP_STAMP(4);
+
     // ---- 6. final masks: S_g = count >= min_collisions restricted to D; T = static keys
     const int64_t cbase = chunk * KCHUNK;  // local index of the chunk's first key
     if (tid < 32) {
@@ -297,13 +336,13 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                 if (widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
             }
         }
-        const float x0 = s_q[g][lane * 4], x1 = s_q[g][lane * 4 + 1], x2 = s_q[g][lane * 4 + 2],
-                    x3 = s_q[g][lane * 4 + 3];
-        const float nn = warp_sum_f(x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3);
-        if (lane == 0) s_qn[g] = sqrtf(nn);
+    }
+    if (tid < G) {
+        s_mrun[tid] = -INFINITY;
+        s_srun[tid] = 0.0f;
     }
     __syncthreads();
-    // ---- 7. compaction (ascending) of U = (union_g S_g) U T; identical in every CTA
+    // ---- 7. compaction (ascending) of U = (union_g S_g) U T; identical in every CTA of the cluster
     if (warp == 0) {
         uint32_t u = s_tm[lane];
 #pragma unroll
@@ -324,33 +363,20 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         if (lane == 31) s_nsel = incl;
     }
     __syncthreads();
-
     MP_STAMP(5);
-    // ---- 8. gather + estimator: entries rank, rank+CS, ...; staged rows, warp per key
-    float m_run[G], s_run[G], acc[G][4];
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        m_run[g] = -INFINITY;
-        s_run[g] = 0.0f;
-        acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0f;
-    }
-    float qv[G][4];
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        qv[g][0] = s_q[g][lane * 4];
-        qv[g][1] = s_q[g][lane * 4 + 1];
-        qv[g][2] = s_q[g][lane * 4 + 2];
-        qv[g][3] = s_q[g][lane * 4 + 3];
-    }
-    const float4 cvec = reinterpret_cast<const float4*>(a.center + unit * HD)[lane];
+
+    // ---- 8. gather + estimator over this CTA's entries (rank, rank+CS, ...), RB keys per batch
     const float* knorm = a.key_norm + unit * a.n_local;
     const uint16_t* kbase = a.k + unit * a.n_local * HD;
     const uint16_t* vbase = a.v + unit * a.n_local * HD;
     const int nsel = s_nsel;
     const int n_mine = nsel > rank ? (nsel - rank + CS - 1) / CS : 0;
     const int nbatch = (n_mine + RB - 1) / RB;
+    float acc[NITEM][2];
+#pragma unroll
+    for (int r = 0; r < NITEM; r++) acc[r][0] = acc[r][1] = 0.0f;
 
-    auto stage = [&](int bt) {  // issue cp.async for batch bt into buffer bt&1
+    auto stage = [&](int bt) {  // cp.async of the K/V rows + |xbar| of batch bt into buffer bt&1
         uint8_t* buf = rows + (bt & 1) * RB * ROWB;
         for (int e = tid; e < RB * 33; e += DEC_THREADS) {
             const int rr = e / 33, part = e % 33;
@@ -374,159 +400,180 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
         __syncthreads();
         const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
-        for (int rr = warp; rr < RB; rr += NWARP) {
-            const int j = bt * RB + rr;
-            if (j >= n_mine) break;
-            const int off = s_list[rank + j * CS];
-            const uint32_t bitm = 1u << (off & 31);
-            const bool is_t = (s_tm[off >> 5] & bitm) != 0;
-            uint32_t inS = 0;
+        const int nb = min(RB, n_mine - bt * RB);
+        // (a) xbar rows = bf16(fl32(k - c)) into the x tile; per-key selection bits and norms
+        for (int e = tid; e < RB * (HD / 2); e += DEC_THREADS) {
+            const int rr = e / (HD / 2), dp = e % (HD / 2);
+            const uint32_t kk = *reinterpret_cast<const uint32_t*>(buf + rr * ROWB + dp * 4);
+            const float k0 = __uint_as_float(kk << 16), k1 = __uint_as_float(kk & 0xffff0000u);
+            const uint32_t x = (uint32_t)f2bf_rn(__fsub_rn(k0, s_c[2 * dp])) |
+                               ((uint32_t)f2bf_rn(__fsub_rn(k1, s_c[2 * dp + 1])) << 16);
+            *reinterpret_cast<uint32_t*>(xt + rr * XS + dp * 4) = x;
+        }
+        if (tid < RB) {
+            uint8_t sb = 0;
+            float xn = 0.0f;
+            if (tid < nb) {
+                const int off = s_list[rank + (bt * RB + tid) * CS];
+                const uint32_t bitm = 1u << (off & 31);
 #pragma unroll
-            for (int g = 0; g < G; g++) inS |= ((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g;
-            const uint8_t* row = buf + rr * ROWB;
-            const uint2 kr = *reinterpret_cast<const uint2*>(row + lane * 8);
-            const uint2 vr = *reinterpret_cast<const uint2*>(row + 256 + lane * 8);
-            const float k0 = __uint_as_float(kr.x << 16), k1 = __uint_as_float(kr.x & 0xffff0000u);
-            const float k2 = __uint_as_float(kr.y << 16), k3 = __uint_as_float(kr.y & 0xffff0000u);
-            const float v0 = __uint_as_float(vr.x << 16), v1 = __uint_as_float(vr.x & 0xffff0000u);
-            const float v2 = __uint_as_float(vr.y << 16), v3 = __uint_as_float(vr.y & 0xffff0000u);
-            float logit[G];
+                for (int g = 0; g < G; g++) sb |= (uint8_t)(((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g);
+                if (s_tm[off >> 5] & bitm) sb |= 0x80;
+                xn = *reinterpret_cast<const float*>(buf + tid * ROWB + 512);
+            }
+            s_sel_k[tid] = sb;
+            s_xn[tid] = xn;
+        }
+        __syncthreads();
+        // (b) logits K Q^T and hashed-vector dots X Q^T on tensor cores (mma.sync m16n8k16)
+        if (warp < 2 * (RB / 16)) {
+            const int mt = warp & 1, which = warp >> 1;  // which: 0 = raw keys (logits), 1 = xbar (cos)
+            const uint8_t* abase = which == 0 ? buf : xt;
+            const int astride = which == 0 ? ROWB : XS;
+            float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const int arow = mt * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+            const uint32_t a_addr = smem_u32(abase + arow * astride + 16 * (lane >> 4));
+            const uint32_t b_addr = smem_u32(s_qb16 + (lane & 7) * QBS + 16 * ((lane >> 3) & 1));
 #pragma unroll
-            for (int g = 0; g < G; g++)
-                logit[g] = warp_sum_f(qv[g][0] * k0 + qv[g][1] * k1 + qv[g][2] * k2 + qv[g][3] * k3) * INV_SQRT_D;
-            float lu[G];
-#pragma unroll
-            for (int g = 0; g < G; g++) lu[g] = 0.0f;
-            if (inS) {
-                // the hashed key vector xbar_i (same arithmetic as the build); |xbar_i| from the index
-                const float x0 = bf2f(f2bf_rn(__fsub_rn(k0, cvec.x))), x1 = bf2f(f2bf_rn(__fsub_rn(k1, cvec.y)));
-                const float x2 = bf2f(f2bf_rn(__fsub_rn(k2, cvec.z))), x3 = bf2f(f2bf_rn(__fsub_rn(k3, cvec.w)));
-                const float xnorm = *reinterpret_cast<const float*>(row + 512);
-#pragma unroll
-                for (int g = 0; g < G; g++) {
-                    if (inS & (1u << g)) {
-                        const float dq = warp_sum_f(qv[g][0] * x0 + qv[g][1] * x1 + qv[g][2] * x2 + qv[g][3] * x3);
-                        const float den = s_qn[g] * xnorm;
-                        float cs = den > 0.0f ? dq / den : 0.0f;
-                        cs = fminf(1.0f, fmaxf(-1.0f, cs));
-                        const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
-                        lu[g] = log_sampling_prob(p, K, a.L, a.minc);
-                    }
+            for (int ks = 0; ks < HD / 16; ks++) {
+                uint32_t af[4], bfr[2];
+                ldsm_x4(af, a_addr + ks * 32);
+                ldsm_x2(bfr, b_addr + ks * 32);
+                mma16816(d4, af, bfr);
+            }
+            float(*dst)[8] = which == 0 ? s_zl : s_zd;
+            const int r0 = mt * 16 + (lane >> 2), c0 = (lane & 3) * 2;
+            dst[r0][c0] = d4[0];
+            dst[r0][c0 + 1] = d4[1];
+            dst[r0 + 8][c0] = d4[2];
+            dst[r0 + 8][c0 + 1] = d4[3];
+        }
+        __syncthreads();
+        // (c) one thread per (key, head): z = q.k/sqrt(d) - log u, u from the angle of the hashed vectors
+        if (tid < RB * G) {
+            const int rr = tid / G, g = tid % G;
+            const uint8_t sb = s_sel_k[rr];
+            float z = -INFINITY;
+            if (rr < nb) {
+                const float logit = s_zl[rr][g] * INV_SQRT_D;
+                if (sb & 0x80) {
+                    z = logit;
+                } else if (sb & (1u << g)) {
+                    const float den = s_qn[g] * s_xn[rr];
+                    float cs = den > 0.0f ? s_zd[rr][g] / den : 0.0f;
+                    cs = fminf(1.0f, fmaxf(-1.0f, cs));
+                    const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
+                    z = logit - log_sampling_prob(p, K, a.L, a.minc);
                 }
             }
-#pragma unroll
-            for (int g = 0; g < G; g++)
-                if (is_t || (inS & (1u << g))) osm_update(logit[g] - lu[g], m_run[g], s_run[g], acc[g], v0, v1, v2, v3);
+            s_w[rr][g] = z;
         }
-        __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2)
+        __syncthreads();
+        // (d) online softmax: batch max per head (warp g), rescale, weights
+        if (warp < G) {
+            const int g = warp;
+            const float z = s_w[lane][g];  // RB == 32: lane = key
+            float mb = z;
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, m));
+            const float mo = s_mrun[g];
+            const float mn = fmaxf(mo, mb);
+            const float sc = (mo == -INFINITY) ? 0.0f : __expf(mo - mn);
+            const float w = (z == -INFINITY) ? 0.0f : __expf(z - mn);
+            const float ws = warp_sum_f(w);
+            s_w[lane][g] = w;
+            if (lane == 0) {
+                s_scale[g] = sc;
+                s_srun[g] = s_srun[g] * sc + ws;
+                s_mrun[g] = mn;
+            }
+        }
+        __syncthreads();
+        // (e) a[g][d] = a * scale + sum_keys w * v   (thread per (head, dim pair))
+#pragma unroll
+        for (int r = 0; r < NITEM; r++) {
+            const int it = tid + r * DEC_THREADS;
+            if (it < G * (HD / 2)) {
+                const int g = it / (HD / 2), dp = it % (HD / 2);
+                const float sc = s_scale[g];
+                float a0 = acc[r][0] * sc, a1 = acc[r][1] * sc;
+                for (int rr = 0; rr < nb; rr++) {
+                    const float w = s_w[rr][g];
+                    const uint32_t vv = *reinterpret_cast<const uint32_t*>(buf + rr * ROWB + 256 + dp * 4);
+                    a0 = fmaf(w, __uint_as_float(vv << 16), a0);
+                    a1 = fmaf(w, __uint_as_float(vv & 0xffff0000u), a1);
+                }
+                acc[r][0] = a0;
+                acc[r][1] = a1;
+            }
+        }
+        __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2); s_w reused
     }
-
     MP_STAMP(6);
-    // ---- 9. warps -> CTA partial per head
+
+    // ---- 9. this CTA's partial state (m, s, a) -> global parts[(cgid * CS + rank)]
+    float* pc = a.parts + (cgid * CS + rank) * G * PART;
 #pragma unroll
-    for (int g = 0; g < G; g++) {
-        if (lane == 0) {
-            s_m[warp][g] = m_run[g];
-            s_s[warp][g] = s_run[g];
+    for (int r = 0; r < NITEM; r++) {
+        const int it = tid + r * DEC_THREADS;
+        if (it < G * (HD / 2)) {
+            const int g = it / (HD / 2), dp = it % (HD / 2);
+            *reinterpret_cast<float2*>(pc + g * PART + 2 + 2 * dp) = make_float2(acc[r][0], acc[r][1]);
         }
-        s_a[warp][lane * 4] = acc[g][0];
-        s_a[warp][lane * 4 + 1] = acc[g][1];
-        s_a[warp][lane * 4 + 2] = acc[g][2];
-        s_a[warp][lane * 4 + 3] = acc[g][3];
-        __syncthreads();
-        if (tid < HD) {
-            const int d = tid;
-            float M = -INFINITY;
-            for (int w = 0; w < NWARP; w++) M = fmaxf(M, s_m[w][g]);
-            float S = 0.0f, A = 0.0f;
-            if (M != -INFINITY) {
-                for (int w = 0; w < NWARP; w++) {
-                    if (s_m[w][g] == -INFINITY) continue;
-                    const float f = __expf(s_m[w][g] - M);
-                    S += s_s[w][g] * f;
-                    A += s_a[w][d] * f;
-                }
-            }
-            s_ca[g][d] = A;
-            if (d == 0) {
-                s_cm[g] = M;
-                s_cs[g] = S;
-            }
-        }
-        __syncthreads();
+    }
+    if (tid < G) {
+        pc[tid * PART] = s_mrun[tid];
+        pc[tid * PART + 1] = s_srun[tid];
     }
     MP_STAMP(7);
-    // ---- 10. cluster partials -> rank 0 -> chunk partial (global)
-    float* pc = a.parts + cgid * G * PART;
-    if (CS > 1) cluster.sync();
-    if (rank == 0) {
-        for (int e = tid; e < G * HD; e += DEC_THREADS) {
-            const int g = e / HD, d = e % HD;
-            float M = -INFINITY;
-            for (int r = 0; r < CS; r++) M = fmaxf(M, *cluster.map_shared_rank(&s_cm[g], r));
-            float S = 0.0f, A = 0.0f;
-            if (M != -INFINITY) {
-                for (int r = 0; r < CS; r++) {
-                    const float mr = *cluster.map_shared_rank(&s_cm[g], r);
-                    if (mr == -INFINITY) continue;
-                    const float f = __expf(mr - M);
-                    S += *cluster.map_shared_rank(&s_cs[g], r) * f;
-                    A += *cluster.map_shared_rank(&s_ca[g][d], r) * f;
-                }
-            }
-            pc[g * PART + 2 + d] = A;
-            if (d == 0) {
-                pc[g * PART] = M;
-                pc[g * PART + 1] = S;
-            }
-        }
-    }
-    if (CS > 1) cluster.sync();  // remote shared memory stays alive until rank 0 has read it
+    if (CS > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     MP_STAMP(8);
-    if (rank != 0) return;
 
-    // ---- 11. last chunk of the unit merges all chunks (fixed order)
+    // ---- 10. the last CTA of the unit merges all nchunks*CS partials (fixed order)
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_flag = atomicAdd(a.unit_ctr + unit, 1u) == (uint32_t)(a.nchunks - 1);
+    if (tid == 0) s_flag = atomicAdd(a.unit_ctr + unit, 1u) == (uint32_t)(a.nchunks * CS - 1);
     __syncthreads();
     if (!s_flag) return;
     __threadfence();
     MP_STAMP(9);
-    const float* pu = a.parts + unit * a.nchunks * G * PART;
-    const int nch = (int)a.nchunks;
-    float* f = reinterpret_cast<float*>(rows);  // reuse the row buffers: [nch][G] scale factors
-    // (a) M_g = max_c m_c,g : warp g, lanes stride over chunks
-    if (warp < G) {
+    const int np = (int)a.nchunks * CS;
+    const float* pu = a.parts + unit * (int64_t)np * G * PART;
+    float* f = reinterpret_cast<float*>(ring);  // [np][G] scale factors (if they fit)
+    const bool fit = (size_t)np * G * 4 <= (size_t)a.ring_bytes;
+    __shared__ float s_M[G], s_S[G];
+    __shared__ int s_cnt[G];
+    if (warp < G) {  // M_g = max_p m_p,g ; count of S_g over chunks
+        const int g = warp;
         float M = -INFINITY;
-        for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(pu + ((int64_t)c * G + warp) * PART));
+        for (int c = lane; c < np; c += 32) M = fmaxf(M, __ldcg(pu + ((int64_t)c * G + g) * PART));
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, m));
-        if (lane == 0) s_cm[warp] = M;
-    }
-    __syncthreads();
-    // (b) f_c,g = e^{m_c,g - M_g};  S_g = sum_c f_c,g s_c,g
-    const bool fit = nch * G * 4 <= 2 * RB * ROWB;
-    if (warp < G) {
-        const float M = s_cm[warp];
+        int cnt = 0;
+        for (int c = lane; c < (int)a.nchunks; c += 32) cnt += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + g);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
         float S = 0.0f;
-        for (int c = lane; c < nch; c += 32) {
-            const float mc = __ldcg(pu + ((int64_t)c * G + warp) * PART);
+        for (int c = lane; c < np; c += 32) {
+            const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
             const float fc = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
-            if (fit) f[c * G + warp] = fc;
-            S += fc * __ldcg(pu + ((int64_t)c * G + warp) * PART + 1);
+            if (fit) f[c * G + g] = fc;
+            S += fc * __ldcg(pu + ((int64_t)c * G + g) * PART + 1);
         }
         S = warp_sum_f(S);
-        if (lane == 0) s_cs[warp] = S;
+        if (lane == 0) {
+            s_M[g] = M;
+            s_S[g] = S;
+            s_cnt[g] = cnt;
+        }
     }
     __syncthreads();
-    // (c) A_g,d = sum_c f_c,g a_c,g,d  (fixed chunk order)
     for (int e = tid; e < G * HD; e += DEC_THREADS) {
         const int g = e / HD, d = e % HD;
-        const float M = s_cm[g], S = s_cs[g];
+        const float M = s_M[g], S = s_S[g];
         float A = 0.0f;
-#pragma unroll 8
-        for (int c = 0; c < nch; c++) {
+#pragma unroll 16
+        for (int c = 0; c < np; c++) {
             float fc;
             if (fit) {
                 fc = f[c * G + g];
@@ -547,11 +594,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
         if (d == 0) {
             if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
-            if (a.s_count) {
-                int tot = 0;
-                for (int c = 0; c < nch; c++) tot += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + g);
-                a.s_count[row] = tot;
-            }
+            if (a.s_count) a.s_count[row] = s_cnt[g];
         }
     }
     if (tid == 0) a.unit_ctr[unit] = 0u;
@@ -588,10 +631,15 @@ int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
+static size_t ring_bytes(int K, int depth) {
+    size_t scan = (size_t)NWARP * depth * qg_of(K) * 512;
+    size_t gath = 2 * RB * ROWB + RB * XS;
+    return (scan > gath ? scan : gath + 127) & ~(size_t)127;
+}
+
 size_t decode_dyn_smem(int K, int G, int ncols_max, int depth, int KLw) {
     size_t qxb = ((size_t)ncols_max * G * 4 + 127) & ~(size_t)127;
-    return qxb + (size_t)NWARP * depth * qg_of(K) * 512 + 2 * RB * ROWB + (size_t)NWARP * depth * 8 +
-           (size_t)G * KLw * 4;
+    return qxb + ring_bytes(K, depth) + (size_t)NWARP * depth * 8 + (size_t)G * KLw * 4;
 }
 
 template <int K, int G>
@@ -601,7 +649,8 @@ static int launch_kg(DecodeArgs a, cudaStream_t st) {
     const int ncols_max = maxg * TG * K;
     a.qx_bytes = (int)(((size_t)ncols_max * G * 4 + 127) & ~(size_t)127);
     a.depth = 3;
-    if (decode_dyn_smem(K, G, ncols_max, 3, a.KLw) > 100 * 1024) a.depth = 2;
+    if (decode_dyn_smem(K, G, ncols_max, 3, a.KLw) > 96 * 1024) a.depth = 2;
+    a.ring_bytes = (int)ring_bytes(K, a.depth);
     size_t smem = decode_dyn_smem(K, G, ncols_max, a.depth, a.KLw);
     auto kern = decode_kernel<K, G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

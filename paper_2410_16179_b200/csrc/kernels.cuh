@@ -42,7 +42,7 @@ struct DecodeArgs {
     int K, L, KL, KLw, KLq, ngroups, TG, QG;
     int64_t nchunks;
     int tsplit, sink, local, minc;
-    int qx_bytes, depth;  // set by the launcher
+    int qx_bytes, depth, ring_bytes;  // set by the launcher
     unsigned long long* timeline;  // debug: [grid][16] globaltimer stamps, or NULL
     float* out;
     float* partial;

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __shared__ float s_zl[RB][8], s_zd[RB][8], s_w[RB][8];
     __shared__ float s_mrun[G], s_srun[G], s_scale[G];
     __shared__ float s_xn[RB];
-    __shared__ uint8_t s_sel_k[RB];  // bit g: key in S_g; bit 7: static
+    __shared__ uint16_t s_sel_k[RB];  // bit g: key in S_g; bit 8: static
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int CS = a.tsplit;
@@ -411,17 +411,17 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
             *reinterpret_cast<uint32_t*>(xt + rr * XS + dp * 4) = x;
         }
         if (tid < RB) {
-            uint8_t sb = 0;
+            uint32_t sb = 0;
             float xn = 0.0f;
             if (tid < nb) {
                 const int off = s_list[rank + (bt * RB + tid) * CS];
                 const uint32_t bitm = 1u << (off & 31);
 #pragma unroll
-                for (int g = 0; g < G; g++) sb |= (uint8_t)(((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g);
-                if (s_tm[off >> 5] & bitm) sb |= 0x80;
+                for (int g = 0; g < G; g++) sb |= ((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g;
+                if (s_tm[off >> 5] & bitm) sb |= 0x100u;
                 xn = *reinterpret_cast<const float*>(buf + tid * ROWB + 512);
             }
-            s_sel_k[tid] = sb;
+            s_sel_k[tid] = (uint16_t)sb;
             s_xn[tid] = xn;
         }
         __syncthreads();
@@ -452,11 +452,11 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         // (c) one thread per (key, head): z = q.k/sqrt(d) - log u, u from the angle of the hashed vectors
         if (tid < RB * G) {
             const int rr = tid / G, g = tid % G;
-            const uint8_t sb = s_sel_k[rr];
+            const uint32_t sb = s_sel_k[rr];
             float z = -INFINITY;
             if (rr < nb) {
                 const float logit = s_zl[rr][g] * INV_SQRT_D;
-                if (sb & 0x80) {
+                if (sb & 0x100u) {
                     z = logit;
                 } else if (sb & (1u << g)) {
                     const float den = s_qn[g] * s_xn[rr];
@@ -539,49 +539,49 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     MP_STAMP(9);
     const int np = (int)a.nchunks * CS;
     const float* pu = a.parts + unit * (int64_t)np * G * PART;
-    float* f = reinterpret_cast<float*>(ring);  // [np][G] scale factors (if they fit)
-    const bool fit = (size_t)np * G * 4 <= (size_t)a.ring_bytes;
-    __shared__ float s_M[G], s_S[G];
     __shared__ int s_cnt[G];
-    if (warp < G) {  // M_g = max_p m_p,g ; count of S_g over chunks
-        const int g = warp;
-        float M = -INFINITY;
-        for (int c = lane; c < np; c += 32) M = fmaxf(M, __ldcg(pu + ((int64_t)c * G + g) * PART));
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, m));
+    if (warp < G) {  // |S_g| summed over the unit's chunks
         int cnt = 0;
-        for (int c = lane; c < (int)a.nchunks; c += 32) cnt += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + g);
+        for (int c = lane; c < (int)a.nchunks; c += 32) cnt += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + warp);
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
-        float S = 0.0f;
-        for (int c = lane; c < np; c += 32) {
-            const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
-            const float fc = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
-            if (fit) f[c * G + g] = fc;
-            S += fc * __ldcg(pu + ((int64_t)c * G + g) * PART + 1);
-        }
-        S = warp_sum_f(S);
-        if (lane == 0) {
-            s_M[g] = M;
-            s_S[g] = S;
-            s_cnt[g] = cnt;
-        }
+        if (lane == 0) s_cnt[warp] = cnt;
     }
-    __syncthreads();
+    // single pass, fixed order p = 0..np-1: all loads of a block of 8 partials are
+    // issued before the (sequential) log-sum-exp combination
     for (int e = tid; e < G * HD; e += DEC_THREADS) {
         const int g = e / HD, d = e % HD;
-        const float M = s_M[g], S = s_S[g];
-        float A = 0.0f;
-#pragma unroll 16
-        for (int c = 0; c < np; c++) {
-            float fc;
-            if (fit) {
-                fc = f[c * G + g];
-            } else {
-                const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
-                fc = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
+        float M = -INFINITY, S = 0.0f, A = 0.0f;
+        for (int c0 = 0; c0 < np; c0 += 8) {
+            float mc[8], sc[8], ac[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const int c = c0 + t;
+                if (c < np) {
+                    const float* pp = pu + ((int64_t)c * G + g) * PART;
+                    mc[t] = __ldcg(pp);
+                    sc[t] = __ldcg(pp + 1);
+                    ac[t] = __ldcg(pp + 2 + d);
+                } else {
+                    mc[t] = -INFINITY;
+                    sc[t] = 0.0f;
+                    ac[t] = 0.0f;
+                }
             }
-            A += fc * __ldcg(pu + ((int64_t)c * G + g) * PART + 2 + d);
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                if (mc[t] == -INFINITY) continue;
+                if (mc[t] > M) {
+                    const float f = (M == -INFINITY) ? 0.0f : __expf(M - mc[t]);
+                    S = S * f + sc[t];
+                    A = A * f + ac[t];
+                    M = mc[t];
+                } else {
+                    const float f = __expf(mc[t] - M);
+                    S += sc[t] * f;
+                    A += ac[t] * f;
+                }
+            }
         }
         const int64_t row = qh0 + g;
         if (a.out) a.out[row * HD + d] = S > 0.0f ? A / S : 0.0f;
@@ -592,11 +592,10 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                 a.partial[row * PART + 1] = S;
             }
         }
-        if (d == 0) {
-            if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
-            if (a.s_count) a.s_count[row] = s_cnt[g];
-        }
+        if (d == 0 && !(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
     }
+    __syncthreads();
+    if (tid < G && a.s_count) a.s_count[qh0 + tid] = s_cnt[tid];
     if (tid == 0) a.unit_ctr[unit] = 0u;
     MP_STAMP(10);
 }

@@ -10,10 +10,10 @@
 namespace mp {
 
 constexpr int QE_COLS = 32;   // columns per CTA (one warp-wide ballot word)
-constexpr int QE_HPB = 16;    // query heads per CTA
+constexpr int QE_HPB = 8;     // query heads per CTA
 constexpr int QE_THREADS = 256;
 
-// CTA = 32 columns x 16 heads; warp w: heads 4*(w%4) .. +3, d-half w/4; lane = column.
+// CTA = 32 columns x 8 heads; warp w: heads 4*(w%2) .. +3, d-quarter w/2; lane = column.
 // fp32 products are exact (bf16 x bf16); fp32 sums certify the sign when
 // |acc| > 2^-16 sum|q_d W_dj| (error <= 65 * 2^-24 * sum|.|); otherwise the
 // warp recomputes that dot in fp64 (certified at 2^-44) and, failing that, in
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
     __shared__ float ws[HD][QE_COLS];
     __shared__ __align__(16) float qs[HD][QE_HPB];
     __shared__ __align__(16) float qa[HD][QE_HPB];
-    __shared__ float pacc[QE_HPB][QE_COLS], pbnd[QE_HPB][QE_COLS];
+    __shared__ float pacc[3][QE_HPB][QE_COLS], pbnd[3][QE_HPB][QE_COLS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j0 = blockIdx.x * QE_COLS;
     const int64_t h0 = (int64_t)blockIdx.y * QE_HPB;
@@ -58,11 +58,11 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
         }
     }
     __syncthreads();
-    const int hs = warp & 3, dh = warp >> 2;
+    const int hs = warp & 1, dq = warp >> 1;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, bnd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll 16
-    for (int dd = 0; dd < HD / 2; dd++) {
-        const int d = dh * (HD / 2) + dd;
+    for (int dd = 0; dd < HD / 4; dd++) {
+        const int d = dq * (HD / 4) + dd;
         const float w = ws[d][lane];
         const float wa = fabsf(w);
         const float4 q4 = *reinterpret_cast<const float4*>(&qs[d][hs * 4]);
@@ -76,22 +76,22 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
         bnd[2] = fmaf(a4.z, wa, bnd[2]);
         bnd[3] = fmaf(a4.w, wa, bnd[3]);
     }
-    if (dh == 1) {
+    if (dq > 0) {
 #pragma unroll
         for (int t = 0; t < 4; t++) {
-            pacc[hs * 4 + t][lane] = acc[t];
-            pbnd[hs * 4 + t][lane] = bnd[t];
+            pacc[dq - 1][hs * 4 + t][lane] = acc[t];
+            pbnd[dq - 1][hs * 4 + t][lane] = bnd[t];
         }
     }
     __syncthreads();
-    if (dh == 1) return;
+    if (dq > 0) return;
     const int j = j0 + lane;
     const bool live = j < KL;
 #pragma unroll
     for (int t = 0; t < 4; t++) {
         const int h = hs * 4 + t;
-        const float s = acc[t] + pacc[h][lane];
-        const float bb = bnd[t] + pbnd[h][lane];
+        const float s = ((acc[t] + pacc[0][h][lane]) + pacc[1][h][lane]) + pacc[2][h][lane];
+        const float bb = ((bnd[t] + pbnd[0][h][lane]) + pbnd[1][h][lane]) + pbnd[2][h][lane];
         int bit = s > 0.0f;
         const bool unsure = live && (h0 + h < BHq) && !(fabsf(s) > 0x1p-16f * bb);
         uint32_t um = __ballot_sync(0xffffffffu, unsure);

@@ -182,6 +182,13 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     uint8_t* myring = ring + (size_t)warp * depth * GB;
     uint64_t* mybar = bars + warp * depth;
     const int n_my = g1 - g0 > warp ? (g1 - g0 - warp + NWARP - 1) / NWARP : 0;
+    if (tid == 0 && g1 > g0) {
+        // the whole code range of this CTA goes to L2 now (HBM streaming overlaps the
+        // query encode); the shared-memory ring below refills from L2
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(csrc + (size_t)g0 * GB),
+                     "r"((uint32_t)((g1 - g0) * GB))
+                     : "memory");
+    }
     if (lane == 0) {
         for (int s = 0; s < depth; s++) mbar_init(mybar + s, 1);
         fence_mbar_init();
@@ -547,52 +554,78 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
         if (lane == 0) s_cnt[warp] = cnt;
     }
-    // single pass, fixed order p = 0..np-1: all loads of a block of 8 partials are
-    // issued before the (sequential) log-sum-exp combination
-    for (int e = tid; e < G * HD; e += DEC_THREADS) {
-        const int g = e / HD, d = e % HD;
-        float M = -INFINITY, S = 0.0f, A = 0.0f;
-        for (int c0 = 0; c0 < np; c0 += 8) {
-            float mc[8], sc[8], ac[8];
+    // (a) stage m, s of every partial in shared memory (one round of loads)
+    float* sm_m = reinterpret_cast<float*>(ring);  // [np][G]
+    float* sm_s = sm_m + (size_t)np * G;           // [np][G]
+    const bool fit = (size_t)np * G * 8 <= (size_t)a.ring_bytes;
+    __shared__ float s_M[G], s_S[G];
+    if (fit) {
+        for (int e = tid; e < np * G; e += DEC_THREADS) {
+            sm_m[e] = __ldcg(pu + (int64_t)e * PART);
+            sm_s[e] = __ldcg(pu + (int64_t)e * PART + 1);
+        }
+    }
+    __syncthreads();
+    // (b) M_g, scale factors f_pg = e^{m_pg - M_g} (in place of m), S_g  (warp g, fixed order)
+    if (warp < G) {
+        const int g = warp;
+        float M = -INFINITY;
+        for (int c = lane; c < np; c += 32)
+            M = fmaxf(M, fit ? sm_m[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART));
 #pragma unroll
-            for (int t = 0; t < 8; t++) {
+        for (int m = 16; m >= 1; m >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, m));
+        float S = 0.0f;
+        for (int c = lane; c < np; c += 32) {
+            const float mc = fit ? sm_m[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART);
+            const float sc = fit ? sm_s[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART + 1);
+            const float f = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
+            if (fit) sm_m[c * G + g] = f;
+            S += f * sc;
+        }
+        S = warp_sum_f(S);
+        if (lane == 0) {
+            s_M[g] = M;
+            s_S[g] = S;
+        }
+    }
+    __syncthreads();
+    // (c) A_g,d = sum_p f_pg a_pg,d: thread per (head, dim pair), 16 partials' loads in flight
+    for (int e = tid; e < G * (HD / 2); e += DEC_THREADS) {
+        const int g = e / (HD / 2), dp = e % (HD / 2);
+        const float M = s_M[g], S = s_S[g];
+        float A0 = 0.0f, A1 = 0.0f;
+        for (int c0 = 0; c0 < np; c0 += 16) {
+            float2 av[16];
+#pragma unroll
+            for (int t = 0; t < 16; t++)
+                av[t] = (c0 + t < np) ? __ldcg(reinterpret_cast<const float2*>(pu + ((int64_t)(c0 + t) * G + g) * PART + 2) + dp)
+                                      : make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int t = 0; t < 16; t++) {
                 const int c = c0 + t;
-                if (c < np) {
-                    const float* pp = pu + ((int64_t)c * G + g) * PART;
-                    mc[t] = __ldcg(pp);
-                    sc[t] = __ldcg(pp + 1);
-                    ac[t] = __ldcg(pp + 2 + d);
+                if (c >= np) break;
+                float f;
+                if (fit) {
+                    f = sm_m[c * G + g];
                 } else {
-                    mc[t] = -INFINITY;
-                    sc[t] = 0.0f;
-                    ac[t] = 0.0f;
+                    const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
+                    f = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
                 }
-            }
-#pragma unroll
-            for (int t = 0; t < 8; t++) {
-                if (mc[t] == -INFINITY) continue;
-                if (mc[t] > M) {
-                    const float f = (M == -INFINITY) ? 0.0f : __expf(M - mc[t]);
-                    S = S * f + sc[t];
-                    A = A * f + ac[t];
-                    M = mc[t];
-                } else {
-                    const float f = __expf(mc[t] - M);
-                    S += sc[t] * f;
-                    A += ac[t] * f;
-                }
+                A0 = fmaf(f, av[t].x, A0);
+                A1 = fmaf(f, av[t].y, A1);
             }
         }
         const int64_t row = qh0 + g;
-        if (a.out) a.out[row * HD + d] = S > 0.0f ? A / S : 0.0f;
+        if (a.out) *reinterpret_cast<float2*>(a.out + row * HD + 2 * dp) = S > 0.0f ? make_float2(A0 / S, A1 / S) : make_float2(0.0f, 0.0f);
         if (a.partial) {
-            a.partial[row * PART + 2 + d] = A;
-            if (d == 0) {
+            a.partial[row * PART + 2 + 2 * dp] = A0;
+            a.partial[row * PART + 3 + 2 * dp] = A1;
+            if (dp == 0) {
                 a.partial[row * PART] = M;
                 a.partial[row * PART + 1] = S;
             }
         }
-        if (d == 0 && !(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
+        if (dp == 0 && !(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
     }
     __syncthreads();
     if (tid < G && a.s_count) a.s_count[qh0 + tid] = s_cnt[tid];

@@ -124,7 +124,9 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     w.status = (uint32_t*)take(256);
     w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
     w.unit_ctr = (uint32_t*)take((size_t)units * 4);
-    w.parts = (float*)take((size_t)units * nch * 8 * G * PART * 4);  // up to 8 CTAs (cluster) per chunk
+    const int64_t nT = n_local < (int64_t)c->sink + c->local ? n_local : (int64_t)c->sink + c->local;
+    const int64_t nst = nT > 0 ? (nT + KCHUNK - 1) / KCHUNK : 1;
+    w.parts = (float*)take((size_t)units * (nch + nst) * 8 * G * PART * 4);  // up to 8 CTAs per cluster
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
     w.bytes = off;
     return w;
@@ -287,6 +289,18 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.TG = g.TG;
     a.QG = g.QG;
     a.nchunks = g.nchunks;
+    {   // static keys T on this shard -> pieces of <= 1024 keys, one cluster each
+        const int64_t lo1 = 0 > -seq_offset ? 0 : -seq_offset;
+        const int64_t hi1 = n_local < (int64_t)cfg->sink - seq_offset ? n_local : (int64_t)cfg->sink - seq_offset;
+        int64_t lo2 = n_global - cfg->local - seq_offset;
+        if (lo2 < 0) lo2 = 0;
+        const int64_t hi2 = n_local < n_global - seq_offset ? n_local : n_global - seq_offset;
+        const int64_t len1 = hi1 > lo1 ? hi1 - lo1 : 0;
+        if (len1 > 0 && lo2 < hi1) lo2 = hi1;
+        const int64_t len2 = hi2 > lo2 ? hi2 - lo2 : 0;
+        const int64_t nT = len1 + len2;
+        a.nstatic = nT > 0 ? (nT + KCHUNK - 1) / KCHUNK : 1;
+    }
     // cluster size: smallest power of two (<= 8) giving >= 1.5 CTAs per SM, with
     // at least 8 table groups (one per warp) per CTA
     const int64_t total = B * Hkv * g.nchunks;

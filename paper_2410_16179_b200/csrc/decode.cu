@@ -113,6 +113,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+__device__ __forceinline__ long long clk64() { return clock64(); }
+#define MP_ACC(ph, t0)                                                                            \
+    do {                                                                                           \
+        if (a.timeline && threadIdx.x == 0) {                                                      \
+            long long t1_ = clk64();                                                               \
+            a.timeline[(size_t)blockIdx.x * 16 + (ph)] += (unsigned long long)(t1_ - (t0));        \
+            t0 = t1_;                                                                              \
+        }                                                                                          \
+    } while (0)
 #define MP_STAMP(ph)                                                                        \
     do {                                                                                     \
         if (a.timeline && threadIdx.x == 0) a.timeline[(size_t)blockIdx.x * 16 + (ph)] = gtimer(); \
@@ -135,6 +144,177 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+// Per-CTA working set of the batched gather (static shared memory).
+template <int G>
+struct GatherShared {
+    int keys[KCHUNK];            // local key index of every entry this CTA gathers
+    uint16_t bits[KCHUNK];       // bit g: key in S_g; bit 8: static (u = 1)
+    uint8_t qb16[8 * QBS];       // query heads as bf16 rows (mma B operand), zero padded
+    float c[HD];                 // centering vector
+    float qn[G];                 // |q_g|
+    float zl[RB][8], zd[RB][8], w[RB][8];
+    float mrun[G], srun[G], scale[G];
+    float xn[RB];
+    uint16_t sbits[RB];
+};
+
+// Batched gather + estimator over n entries (keys[], bits[]) of one unit
+// (PAPER.md:109-115): K/V rows and |xbar| staged by cp.async, logits K Q^T and
+// hashed-vector dots X Q^T on tensor cores (mma.sync m16n8k16, bf16 in, fp32
+// accumulate), one thread per (key, head) for z = logit - log u, then an online
+// softmax whose state (m, s per head; a per (head, dim pair)) is thread-parallel.
+template <int K, int G>
+__device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared<G>& sh, uint8_t* region,
+                                               int n, int64_t unit, float (&acc)[(G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS][2]) {
+    constexpr int NITEM = (G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint8_t* rows = region;                  // [2][RB][ROWB]
+    uint8_t* xt = region + 2 * RB * ROWB;    // [RB][XS]
+    const float* knorm = a.key_norm + unit * a.n_local;
+    const uint16_t* kbase = a.k + unit * a.n_local * HD;
+    const uint16_t* vbase = a.v + unit * a.n_local * HD;
+    const int nbatch = (n + RB - 1) / RB;
+    auto stage = [&](int bt) {
+        uint8_t* buf = rows + (bt & 1) * RB * ROWB;
+        for (int e = tid; e < RB * 33; e += DEC_THREADS) {
+            const int rr = e / 33, part = e % 33;
+            const int j = bt * RB + rr;
+            if (j >= n) continue;
+            const int64_t i = sh.keys[j];
+            uint8_t* dst = buf + rr * ROWB;
+            if (part < 16) cp_async16(dst + part * 16, kbase + i * HD + part * 8);
+            else if (part < 32) cp_async16(dst + 256 + (part - 16) * 16, vbase + i * HD + (part - 16) * 8);
+            else cp_async4(dst + 512, knorm + i);
+        }
+        cp_async_commit();
+    };
+    if (nbatch > 0) stage(0);
+    long long tcl = clk64();
+    for (int bt = 0; bt < nbatch; bt++) {
+        if (bt + 1 < nbatch) {
+            stage(bt + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        MP_ACC(11, tcl);
+        const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
+        const int nb = min(RB, n - bt * RB);
+        // (a) xbar = bf16(fl32(k - c)), 8 dims per task; per-row selection bits and |xbar|
+        for (int e = tid; e < RB * (HD / 8); e += DEC_THREADS) {
+            const int rr = e / (HD / 8), dg = e % (HD / 8);
+            const uint4 kv = *reinterpret_cast<const uint4*>(buf + rr * ROWB + dg * 16);
+            const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+            uint32_t xw[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const float k0 = __uint_as_float(kw[t] << 16), k1 = __uint_as_float(kw[t] & 0xffff0000u);
+                xw[t] = (uint32_t)f2bf_rn(__fsub_rn(k0, sh.c[dg * 8 + 2 * t])) |
+                        ((uint32_t)f2bf_rn(__fsub_rn(k1, sh.c[dg * 8 + 2 * t + 1])) << 16);
+            }
+            *reinterpret_cast<uint4*>(xt + rr * XS + dg * 16) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+        }
+        if (tid < RB) {
+            const bool live = tid < nb;
+            sh.sbits[tid] = live ? sh.bits[bt * RB + tid] : (uint16_t)0;
+            sh.xn[tid] = live ? *reinterpret_cast<const float*>(buf + tid * ROWB + 512) : 0.0f;
+        }
+        __syncthreads();
+        MP_ACC(12, tcl);
+        // (b) logits and hashed-vector dots on tensor cores
+        if (warp < 2 * (RB / 16)) {
+            const int mt = warp & 1, which = warp >> 1;  // 0: raw keys (logits), 1: xbar (cos)
+            const uint8_t* abase = which == 0 ? buf : xt;
+            const int astride = which == 0 ? ROWB : XS;
+            float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const int arow = mt * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+            const uint32_t a_addr = smem_u32(abase + arow * astride + 16 * (lane >> 4));
+            const uint32_t b_addr = smem_u32(sh.qb16 + (lane & 7) * QBS + 16 * ((lane >> 3) & 1));
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ks++) {
+                uint32_t af[4], bfr[2];
+                ldsm_x4(af, a_addr + ks * 32);
+                ldsm_x2(bfr, b_addr + ks * 32);
+                mma16816(d4, af, bfr);
+            }
+            float(*dst)[8] = which == 0 ? sh.zl : sh.zd;
+            const int r0 = mt * 16 + (lane >> 2), c0 = (lane & 3) * 2;
+            dst[r0][c0] = d4[0];
+            dst[r0][c0 + 1] = d4[1];
+            dst[r0 + 8][c0] = d4[2];
+            dst[r0 + 8][c0 + 1] = d4[3];
+        }
+        __syncthreads();
+        MP_ACC(13, tcl);
+        // (c) one thread per (key, head): z = q.k/sqrt(d) - log u; u from the hashed vectors' angle (R5)
+        for (int it = tid; it < RB * G; it += DEC_THREADS) {
+            const int rr = it / G, g = it % G;
+            const uint32_t sb = sh.sbits[rr];
+            float z = -INFINITY;
+            if (rr < nb) {
+                const float logit = sh.zl[rr][g] * INV_SQRT_D;
+                if (sb & 0x100u) {
+                    z = logit;
+                } else if (sb & (1u << g)) {
+                    const float den = sh.qn[g] * sh.xn[rr];
+                    float cs = den > 0.0f ? sh.zd[rr][g] / den : 0.0f;
+                    cs = fminf(1.0f, fmaxf(-1.0f, cs));
+                    const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
+                    z = logit - log_sampling_prob(p, K, a.L, a.minc);
+                }
+            }
+            sh.w[rr][g] = z;
+        }
+        __syncthreads();
+        MP_ACC(14, tcl);
+        // (d) online softmax: batch max per head (warp g), rescale factor, weights
+        if (warp < G) {
+            const int g = warp;
+            const float z = sh.w[lane][g];  // RB == 32: lane = row
+            float mb = z;
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, m));
+            const float mo = sh.mrun[g];
+            const float mn = fmaxf(mo, mb);
+            const float sc = (mo == -INFINITY) ? 0.0f : __expf(mo - mn);
+            const float w = (z == -INFINITY) ? 0.0f : __expf(z - mn);
+            const float wsum = warp_sum_f(w);
+            sh.w[lane][g] = w;
+            if (lane == 0) {
+                sh.scale[g] = sc;
+                sh.srun[g] = sh.srun[g] * sc + wsum;
+                sh.mrun[g] = mn;
+            }
+        }
+        __syncthreads();
+        // (e) a[g][d] = a * scale + sum_rows w * v  (4 independent partial sums per item)
+#pragma unroll
+        for (int r = 0; r < NITEM; r++) {
+            const int it = tid + r * DEC_THREADS;
+            if (it < G * (HD / 2)) {
+                const int g = it / (HD / 2), dp = it % (HD / 2);
+                float p0[4] = {0.0f, 0.0f, 0.0f, 0.0f}, p1[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                for (int r0 = 0; r0 < nb; r0 += 4) {
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const int rr = r0 + t;
+                        const float w = rr < nb ? sh.w[rr][g] : 0.0f;
+                        const uint32_t vv = *reinterpret_cast<const uint32_t*>(buf + (rr < RB ? rr : 0) * ROWB + 256 + dp * 4);
+                        p0[t] = fmaf(w, __uint_as_float(vv << 16), p0[t]);
+                        p1[t] = fmaf(w, __uint_as_float(vv & 0xffff0000u), p1[t]);
+                    }
+                }
+                const float sc = sh.scale[g];
+                acc[r][0] = acc[r][0] * sc + ((p0[0] + p0[1]) + (p0[2] + p0[3]));
+                acc[r][1] = acc[r][1] * sc + ((p1[0] + p1[1]) + (p1[2] + p1[3]));
+            }
+        }
+        __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2); w reused
+        MP_ACC(15, tcl);
+    }
+}
+
 template <int K, int G>
 __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     constexpr int TG = tg_of(K), QG = qg_of(K);
@@ -143,31 +323,26 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     extern __shared__ __align__(128) uint8_t dsm[];
     uint32_t* qx = reinterpret_cast<uint32_t*>(dsm);  // [ncols][G] match masks
     uint8_t* ring = dsm + a.qx_bytes;                  // scan: [NWARP][depth][GB]; gather: rows + x tile
-    uint8_t* rows = ring;                              // [2][RB][ROWB]
-    uint8_t* xt = ring + 2 * RB * ROWB;                // [RB][XS] bf16 xbar rows
     uint64_t* bars = reinterpret_cast<uint64_t*>(ring + a.ring_bytes);  // [NWARP][depth]
     uint32_t* qb = reinterpret_cast<uint32_t*>(bars + NWARP * a.depth);  // [G][KLw] packed query bits
 
     __shared__ uint32_t s_part[NWARP][G][2][32];
     __shared__ uint32_t s_sel[G][32];
     __shared__ uint32_t s_tm[32];
-    __shared__ uint16_t s_list[KCHUNK];
-    __shared__ int s_nsel;
+    __shared__ int s_n;
     __shared__ uint32_t s_flag;
-    __shared__ __align__(16) uint8_t s_qb16[8 * QBS];  // query heads as bf16 rows (B operand), zero padded
-    __shared__ float s_c[HD];
-    __shared__ float s_qn[G];
-    __shared__ float s_zl[RB][8], s_zd[RB][8], s_w[RB][8];
-    __shared__ float s_mrun[G], s_srun[G], s_scale[G];
-    __shared__ float s_xn[RB];
-    __shared__ uint16_t s_sel_k[RB];  // bit g: key in S_g; bit 8: static
+    __shared__ GatherShared<G> sh;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int CS = a.tsplit;
     cgr::cluster_group cluster = cgr::this_cluster();
     const int rank = CS > 1 ? (int)cluster.block_rank() : 0;
-    const int64_t cgid = blockIdx.x / CS;  // global chunk = unit * nchunks + chunk
-    const int64_t unit = cgid / a.nchunks, chunk = cgid % a.nchunks;
+    const int64_t per_unit = a.nchunks + a.nstatic;  // clusters per unit: chunk scans + static pieces
+    const int64_t cid = blockIdx.x / CS;
+    const int64_t unit = cid / per_unit, slot = cid % per_unit;
+    const bool is_static = slot >= a.nchunks;
+    const int64_t chunk = slot;
+    const int64_t cgid = unit * a.nchunks + chunk;  // global chunk (valid if !is_static)
     const int64_t b = unit / a.Hkv, hkv = unit % a.Hkv;
     const int64_t qh0 = b * a.Hq + hkv * G;  // first query head (row of q) of this unit
     const int g0 = (int)((int64_t)rank * a.ngroups / CS);
@@ -177,349 +352,240 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     const int depth = a.depth;
     MP_STAMP(0);
 
-    // ---- 1. start streaming this warp's code groups (independent of the query)
     const uint8_t* csrc = reinterpret_cast<const uint8_t*>(a.codes) + (size_t)cgid * a.KLq * 512;
     uint8_t* myring = ring + (size_t)warp * depth * GB;
     uint64_t* mybar = bars + warp * depth;
-    const int n_my = g1 - g0 > warp ? (g1 - g0 - warp + NWARP - 1) / NWARP : 0;
-    if (tid == 0 && g1 > g0) {
-        // the whole code range of this CTA goes to L2 now (HBM streaming overlaps the
-        // query encode); the shared-memory ring below refills from L2
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(csrc + (size_t)g0 * GB),
-                     "r"((uint32_t)((g1 - g0) * GB))
-                     : "memory");
-    }
-    if (lane == 0) {
-        for (int s = 0; s < depth; s++) mbar_init(mybar + s, 1);
-        fence_mbar_init();
-        for (int k = 0; k < depth && k < n_my; k++) {
-            const int grp = g0 + warp + k * NWARP;
-            mbar_arrive_expect_tx(mybar + k, GB);
-            bulk_g2s(myring + k * GB, csrc + (size_t)grp * GB, GB, mybar + k);
+    const int n_my = (!is_static && g1 - g0 > warp) ? (g1 - g0 - warp + NWARP - 1) / NWARP : 0;
+    if (!is_static) {
+        // ---- 1. stream this CTA's code groups: whole range -> L2 now, ring refills from L2
+        if (tid == 0 && g1 > g0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(csrc + (size_t)g0 * GB),
+                         "r"((uint32_t)((g1 - g0) * GB))
+                         : "memory");
+        if (lane == 0) {
+            for (int s = 0; s < depth; s++) mbar_init(mybar + s, 1);
+            fence_mbar_init();
+            for (int k = 0; k < depth && k < n_my; k++) {
+                const int grp = g0 + warp + k * NWARP;
+                mbar_arrive_expect_tx(mybar + k, GB);
+                bulk_g2s(myring + k * GB, csrc + (size_t)grp * GB, GB, mybar + k);
+            }
         }
     }
-    // query rows (bf16 B operand, heads >= G zero) and centering vector: no dependency on the encode
+    // query rows (bf16 mma operand, heads >= G zero), |q_g|, centering vector: no dependency on the encode
     for (int e = tid; e < 8 * (HD / 2); e += DEC_THREADS) {
         const int g = e / (HD / 2), dp = e % (HD / 2);
         uint32_t v = 0;
         if (g < G) v = __ldg(reinterpret_cast<const uint32_t*>(a.q + (qh0 + g) * HD) + dp);
-        *reinterpret_cast<uint32_t*>(s_qb16 + g * QBS + dp * 4) = v;
+        *reinterpret_cast<uint32_t*>(sh.qb16 + g * QBS + dp * 4) = v;
     }
-    if (tid < HD) s_c[tid] = __ldg(a.center + unit * HD + tid);
-    __syncwarp();
-
-    // ---- 2. wait for the query-encode kernel (programmatic dependent launch)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    MP_STAMP(1);
-
-    // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
-    for (int e = tid; e < G * a.KLw; e += DEC_THREADS) qb[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
+    if (tid < HD) sh.c[tid] = __ldg(a.center + unit * HD + tid);
+    if (tid < G) {
+        sh.mrun[tid] = -INFINITY;
+        sh.srun[tid] = 0.0f;
+    }
     __syncthreads();
-    for (int e = tid; e < ncols * G; e += DEC_THREADS) {
-        const int c = e / G, g = e % G;
-        const int col = col0 + c;
-        uint32_t bit = 0;
-        if (col < a.KL) bit = (qb[g * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
-        qx[e] = bit ? 0u : 0xffffffffu;
-    }
-    if (tid < G * 32) {  // |q_g|
+    if (tid < G * 32) {
         const int g = tid >> 5;
-        const uint2 qq = *reinterpret_cast<const uint2*>(s_qb16 + g * QBS + lane * 8);
+        const uint2 qq = *reinterpret_cast<const uint2*>(sh.qb16 + g * QBS + lane * 8);
         const float x0 = __uint_as_float(qq.x << 16), x1 = __uint_as_float(qq.x & 0xffff0000u);
         const float x2 = __uint_as_float(qq.y << 16), x3 = __uint_as_float(qq.y & 0xffff0000u);
         const float nn = warp_sum_f(x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3);
-        if (lane == 0) s_qn[g] = sqrtf(nn);
+        if (lane == 0) sh.qn[g] = sqrtf(nn);
     }
-    __syncthreads();
-    MP_STAMP(2);
 
-    // ---- 4. scan
-    uint32_t s1[G], s2[G];
-#pragma unroll
-    for (int g = 0; g < G; g++) s1[g] = s2[g] = 0u;
-    for (int k = 0; k < n_my; k++) {
-        const int slot = k % depth;
-        const int grp = g0 + warp + k * NWARP;
-        mbar_wait(mybar + slot, (uint32_t)((k / depth) & 1));
-        uint4 P[QG];
-        const uint4* src = reinterpret_cast<const uint4*>(myring + slot * GB) + lane;
-#pragma unroll
-        for (int t = 0; t < QG; t++) P[t] = src[t * 32];
-        __syncwarp();
-        if (lane == 0 && k + depth < n_my) {
-            fence_proxy_async();
-            const int ng = grp + depth * NWARP;
-            mbar_arrive_expect_tx(mybar + slot, GB);
-            bulk_g2s(myring + slot * GB, csrc + (size_t)ng * GB, GB, mybar + slot);
+    if (is_static) {
+        // ---- static piece: keys of T = [0,sink) U [n-local,n) (global positions) on this shard,
+        // u = 1 (P:115 log [u, 1_t]); no dependency on the query codes
+        const int64_t off = a.seq_offset, nl = a.n_local;
+        const int64_t lo1 = max((int64_t)0, -off), hi1 = min(nl, (int64_t)a.sink - off);
+        const int64_t len1 = hi1 > lo1 ? hi1 - lo1 : 0;
+        int64_t lo2 = max((int64_t)0, a.n_global - a.local - off), hi2 = min(nl, a.n_global - off);
+        if (len1 > 0 && lo2 < hi1) lo2 = hi1;
+        const int64_t len2 = hi2 > lo2 ? hi2 - lo2 : 0;
+        const int64_t p0 = (slot - a.nchunks) * (int64_t)KCHUNK;  // this piece's first T entry
+        const int64_t nT = len1 + len2;
+        const int64_t cnt = nT > p0 ? min((int64_t)KCHUNK, nT - p0) : 0;
+        const int nmine = cnt > rank ? (int)((cnt - rank + CS - 1) / CS) : 0;
+        for (int j = tid; j < nmine; j += DEC_THREADS) {
+            const int64_t t = p0 + rank + (int64_t)j * CS;
+            sh.keys[j] = (int)(t < len1 ? lo1 + t : lo2 + (t - len1));
+            sh.bits[j] = 0x100u;
         }
-        const uint32_t* wv = reinterpret_cast<const uint32_t*>(P);
-        const uint32_t* qrow = qx + (size_t)(grp - g0) * TG * K * G;
+        if (tid == 0) s_n = nmine;
+        __syncthreads();
+    } else {
+        // ---- 2. wait for the query-encode kernel (programmatic dependent launch)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        MP_STAMP(1);
+        // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
+        for (int e = tid; e < G * a.KLw; e += DEC_THREADS) qb[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
+        __syncthreads();
+        for (int e = tid; e < ncols * G; e += DEC_THREADS) {
+            const int c = e / G, g = e % G;
+            const int col = col0 + c;
+            uint32_t bit = 0;
+            if (col < a.KL) bit = (qb[g * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
+            qx[e] = bit ? 0u : 0xffffffffu;
+        }
+        __syncthreads();
+        MP_STAMP(2);
+
+        // ---- 4. scan
+        uint32_t s1[G], s2[G];
 #pragma unroll
-        for (int tt = 0; tt < TG; tt++) {
-            if (grp * TG + tt < a.L) {
-                uint32_t m[G];
+        for (int g = 0; g < G; g++) s1[g] = s2[g] = 0u;
+        for (int k = 0; k < n_my; k++) {
+            const int sl = k % depth;
+            const int grp = g0 + warp + k * NWARP;
+            mbar_wait(mybar + sl, (uint32_t)((k / depth) & 1));
+            uint4 P[QG];
+            const uint4* src = reinterpret_cast<const uint4*>(myring + sl * GB) + lane;
 #pragma unroll
-                for (int g = 0; g < G; g++) m[g] = 0xffffffffu;
+            for (int t = 0; t < QG; t++) P[t] = src[t * 32];
+            __syncwarp();
+            if (lane == 0 && k + depth < n_my) {
+                fence_proxy_async();
+                const int ng = grp + depth * NWARP;
+                mbar_arrive_expect_tx(mybar + sl, GB);
+                bulk_g2s(myring + sl * GB, csrc + (size_t)ng * GB, GB, mybar + sl);
+            }
+            const uint32_t* wv = reinterpret_cast<const uint32_t*>(P);
+            const uint32_t* qrow = qx + (size_t)(grp - g0) * TG * K * G;
 #pragma unroll
-                for (int bb = 0; bb < K; bb++) {
-                    const uint32_t w = wv[tt * K + bb];
-                    uint32_t qq[G];
-                    load_masks<G>(qrow + (tt * K + bb) * G, qq);
+            for (int tt = 0; tt < TG; tt++) {
+                if (grp * TG + tt < a.L) {
+                    uint32_t m[G];
 #pragma unroll
-                    for (int g = 0; g < G; g++) m[g] &= w ^ qq[g];
-                }
+                    for (int g = 0; g < G; g++) m[g] = 0xffffffffu;
 #pragma unroll
-                for (int g = 0; g < G; g++) {
-                    s2[g] |= s1[g] & m[g];
-                    s1[g] |= m[g];
+                    for (int bb = 0; bb < K; bb++) {
+                        const uint32_t w = wv[tt * K + bb];
+                        uint32_t qq[G];
+                        load_masks<G>(qrow + (tt * K + bb) * G, qq);
+#pragma unroll
+                        for (int g = 0; g < G; g++) m[g] &= w ^ qq[g];
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        s2[g] |= s1[g] & m[g];
+                        s1[g] |= m[g];
+                    }
                 }
             }
         }
-    }
 
-    // ---- 5. combine: warps -> CTA (shared), CTAs -> cluster (DSMEM)
+        // ---- 5. combine: warps -> CTA (shared), CTAs -> cluster (DSMEM)
 #pragma unroll
-    for (int g = 0; g < G; g++) {
-        s_part[warp][g][0][lane] = s1[g];
-        s_part[warp][g][1][lane] = s2[g];
-    }
-    __syncthreads();
-    MP_STAMP(3);
-    uint32_t f1 = 0, f2 = 0;  // valid in threads tid < G*32: (g = tid/32, block = lane)
-    if (tid < G * 32) {
-        const int g = tid >> 5;
-        for (int w = 0; w < NWARP; w++) {
-            const uint32_t b1 = s_part[w][g][0][lane], b2 = s_part[w][g][1][lane];
-            f2 |= b2 | (f1 & b1);
-            f1 |= b1;
+        for (int g = 0; g < G; g++) {
+            s_part[warp][g][0][lane] = s1[g];
+            s_part[warp][g][1][lane] = s2[g];
         }
-    }
-    __syncthreads();
-    if (tid < G * 32) {
-        s_part[0][tid >> 5][0][lane] = f1;
-        s_part[0][tid >> 5][1][lane] = f2;
-    }
-    if (CS > 1) {
-        cluster.sync();
+        __syncthreads();
+        MP_STAMP(3);
+        uint32_t f1 = 0, f2 = 0;  // valid in threads tid < G*32: (g = tid/32, block = lane)
         if (tid < G * 32) {
             const int g = tid >> 5;
-            f1 = f2 = 0;
-            for (int r = 0; r < CS; r++) {
-                const uint32_t* rp = cluster.map_shared_rank(&s_part[0][g][0][0], r);
-                const uint32_t b1 = rp[lane], b2 = rp[32 + lane];
+            for (int w = 0; w < NWARP; w++) {
+                const uint32_t b1 = s_part[w][g][0][lane], b2 = s_part[w][g][1][lane];
                 f2 |= b2 | (f1 & b1);
                 f1 |= b1;
             }
         }
-        // remote reads done: let the peers go on; we wait for them only before exiting
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    }
-    MP_STAMP(4);
-
-    // ---- 6. final masks: S_g = count >= min_collisions restricted to D; T = static keys
-    const int64_t cbase = chunk * KCHUNK;  // local index of the chunk's first key
-    if (tid < 32) {
-        const int64_t base = cbase + lane * 32;
-        const uint32_t valid = range_mask(base, 0, a.n_local);
-        s_tm[lane] = (range_mask(base, -a.seq_offset, (int64_t)a.sink - a.seq_offset) |
-                      range_mask(base, a.n_global - a.local - a.seq_offset, a.n_global - a.seq_offset)) &
-                     valid;
-    }
-    __syncthreads();
-    if (tid < G * 32) {
-        const int g = tid >> 5;
-        uint32_t v = (a.minc == 1 ? f1 : f2);
-        const int64_t base = cbase + lane * 32;
-        v &= range_mask(base, 0, a.n_local) & ~s_tm[lane];
-        s_sel[g][lane] = v;
-        if (rank == 0) {
-            int cnt = __popc(v);
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
-            if (lane == 0) a.chunk_cnt[cgid * G + g] = cnt;
-            if (a.s_mask) {
-                const int64_t nw = (a.n_local + 31) >> 5;
-                const int64_t widx = chunk * 32 + lane;
-                if (widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
+        __syncthreads();
+        if (tid < G * 32) {
+            s_part[0][tid >> 5][0][lane] = f1;
+            s_part[0][tid >> 5][1][lane] = f2;
+        }
+        if (CS > 1) {
+            cluster.sync();
+            if (tid < G * 32) {
+                const int g = tid >> 5;
+                f1 = f2 = 0;
+                for (int r = 0; r < CS; r++) {
+                    const uint32_t* rp = cluster.map_shared_rank(&s_part[0][g][0][0], r);
+                    const uint32_t b1 = rp[lane], b2 = rp[32 + lane];
+                    f2 |= b2 | (f1 & b1);
+                    f1 |= b1;
+                }
             }
         }
-    }
-    if (tid < G) {
-        s_mrun[tid] = -INFINITY;
-        s_srun[tid] = 0.0f;
-    }
-    __syncthreads();
-    // ---- 7. compaction (ascending) of U = (union_g S_g) U T; identical in every CTA of the cluster
-    if (warp == 0) {
-        uint32_t u = s_tm[lane];
-#pragma unroll
-        for (int g = 0; g < G; g++) u |= s_sel[g][lane];
-        const int c = __popc(u);
-        int incl = c;
-#pragma unroll
-        for (int m = 1; m < 32; m <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, m);
-            if (lane >= m) incl += t;
+        MP_STAMP(4);
+
+        // ---- 6. final masks: S_g = count >= min_collisions restricted to D (T excluded)
+        const int64_t cbase = chunk * KCHUNK;  // local index of the chunk's first key
+        if (tid < 32) {
+            const int64_t base = cbase + lane * 32;
+            const uint32_t valid = range_mask(base, 0, a.n_local);
+            s_tm[lane] = (range_mask(base, -a.seq_offset, (int64_t)a.sink - a.seq_offset) |
+                          range_mask(base, a.n_global - a.local - a.seq_offset, a.n_global - a.seq_offset)) &
+                         valid;
         }
-        int pos = incl - c;
-        while (u) {
-            const int r = __ffs(u) - 1;
-            u &= u - 1;
-            s_list[pos++] = (uint16_t)(lane * 32 + r);
+        __syncthreads();
+        if (tid < G * 32) {
+            const int g = tid >> 5;
+            uint32_t v = (a.minc == 1 ? f1 : f2);
+            const int64_t base = cbase + lane * 32;
+            v &= range_mask(base, 0, a.n_local) & ~s_tm[lane];
+            s_sel[g][lane] = v;
+            if (rank == 0) {
+                int cnt = __popc(v);
+#pragma unroll
+                for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
+                if (lane == 0) a.chunk_cnt[cgid * G + g] = cnt;
+                if (a.s_mask) {
+                    const int64_t nw = (a.n_local + 31) >> 5;
+                    const int64_t widx = chunk * 32 + lane;
+                    if (widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
+                }
+            }
         }
-        if (lane == 31) s_nsel = incl;
+        __syncthreads();
+        // ---- 7. compaction (ascending) of union_g S_g; entry e goes to cluster rank e % CS
+        if (warp == 0) {
+            uint32_t u = 0;
+#pragma unroll
+            for (int g = 0; g < G; g++) u |= s_sel[g][lane];
+            const int c = __popc(u);
+            int incl = c;
+#pragma unroll
+            for (int m = 1; m < 32; m <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, m);
+                if (lane >= m) incl += t;
+            }
+            int pos = incl - c;
+            while (u) {
+                const int r = __ffs(u) - 1;
+                u &= u - 1;
+                if (pos % CS == rank) {
+                    const int j = pos / CS;
+                    const uint32_t bitm = 1u << r;
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int g = 0; g < G; g++) bits |= ((s_sel[g][lane] & bitm) ? 1u : 0u) << g;
+                    sh.keys[j] = (int)(cbase + lane * 32 + r);
+                    sh.bits[j] = (uint16_t)bits;
+                }
+                pos++;
+            }
+            if (lane == 31) s_n = incl > rank ? (incl - rank + CS - 1) / CS : 0;
+        }
+        // remote s_part reads are done: let the cluster peers go on (we wait before exiting)
+        if (CS > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        __syncthreads();
     }
-    __syncthreads();
     MP_STAMP(5);
 
-    // ---- 8. gather + estimator over this CTA's entries (rank, rank+CS, ...), RB keys per batch
-    const float* knorm = a.key_norm + unit * a.n_local;
-    const uint16_t* kbase = a.k + unit * a.n_local * HD;
-    const uint16_t* vbase = a.v + unit * a.n_local * HD;
-    const int nsel = s_nsel;
-    const int n_mine = nsel > rank ? (nsel - rank + CS - 1) / CS : 0;
-    const int nbatch = (n_mine + RB - 1) / RB;
+    // ---- 8. gather + estimator over this CTA's entries
     float acc[NITEM][2];
 #pragma unroll
     for (int r = 0; r < NITEM; r++) acc[r][0] = acc[r][1] = 0.0f;
-
-    auto stage = [&](int bt) {  // cp.async of the K/V rows + |xbar| of batch bt into buffer bt&1
-        uint8_t* buf = rows + (bt & 1) * RB * ROWB;
-        for (int e = tid; e < RB * 33; e += DEC_THREADS) {
-            const int rr = e / 33, part = e % 33;
-            const int j = bt * RB + rr;
-            if (j >= n_mine) continue;
-            const int64_t i = cbase + s_list[rank + j * CS];
-            uint8_t* dst = buf + rr * ROWB;
-            if (part < 16) cp_async16(dst + part * 16, kbase + i * HD + part * 8);
-            else if (part < 32) cp_async16(dst + 256 + (part - 16) * 16, vbase + i * HD + (part - 16) * 8);
-            else cp_async4(dst + 512, knorm + i);
-        }
-        cp_async_commit();
-    };
-    if (nbatch > 0) stage(0);
-    for (int bt = 0; bt < nbatch; bt++) {
-        if (bt + 1 < nbatch) {
-            stage(bt + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
-        const int nb = min(RB, n_mine - bt * RB);
-        // (a) xbar rows = bf16(fl32(k - c)) into the x tile; per-key selection bits and norms
-        for (int e = tid; e < RB * (HD / 2); e += DEC_THREADS) {
-            const int rr = e / (HD / 2), dp = e % (HD / 2);
-            const uint32_t kk = *reinterpret_cast<const uint32_t*>(buf + rr * ROWB + dp * 4);
-            const float k0 = __uint_as_float(kk << 16), k1 = __uint_as_float(kk & 0xffff0000u);
-            const uint32_t x = (uint32_t)f2bf_rn(__fsub_rn(k0, s_c[2 * dp])) |
-                               ((uint32_t)f2bf_rn(__fsub_rn(k1, s_c[2 * dp + 1])) << 16);
-            *reinterpret_cast<uint32_t*>(xt + rr * XS + dp * 4) = x;
-        }
-        if (tid < RB) {
-            uint32_t sb = 0;
-            float xn = 0.0f;
-            if (tid < nb) {
-                const int off = s_list[rank + (bt * RB + tid) * CS];
-                const uint32_t bitm = 1u << (off & 31);
-#pragma unroll
-                for (int g = 0; g < G; g++) sb |= ((s_sel[g][off >> 5] & bitm) ? 1u : 0u) << g;
-                if (s_tm[off >> 5] & bitm) sb |= 0x100u;
-                xn = *reinterpret_cast<const float*>(buf + tid * ROWB + 512);
-            }
-            s_sel_k[tid] = (uint16_t)sb;
-            s_xn[tid] = xn;
-        }
-        __syncthreads();
-        // (b) logits K Q^T and hashed-vector dots X Q^T on tensor cores (mma.sync m16n8k16)
-        if (warp < 2 * (RB / 16)) {
-            const int mt = warp & 1, which = warp >> 1;  // which: 0 = raw keys (logits), 1 = xbar (cos)
-            const uint8_t* abase = which == 0 ? buf : xt;
-            const int astride = which == 0 ? ROWB : XS;
-            float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-            const int arow = mt * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
-            const uint32_t a_addr = smem_u32(abase + arow * astride + 16 * (lane >> 4));
-            const uint32_t b_addr = smem_u32(s_qb16 + (lane & 7) * QBS + 16 * ((lane >> 3) & 1));
-#pragma unroll
-            for (int ks = 0; ks < HD / 16; ks++) {
-                uint32_t af[4], bfr[2];
-                ldsm_x4(af, a_addr + ks * 32);
-                ldsm_x2(bfr, b_addr + ks * 32);
-                mma16816(d4, af, bfr);
-            }
-            float(*dst)[8] = which == 0 ? s_zl : s_zd;
-            const int r0 = mt * 16 + (lane >> 2), c0 = (lane & 3) * 2;
-            dst[r0][c0] = d4[0];
-            dst[r0][c0 + 1] = d4[1];
-            dst[r0 + 8][c0] = d4[2];
-            dst[r0 + 8][c0 + 1] = d4[3];
-        }
-        __syncthreads();
-        // (c) one thread per (key, head): z = q.k/sqrt(d) - log u, u from the angle of the hashed vectors
-        if (tid < RB * G) {
-            const int rr = tid / G, g = tid % G;
-            const uint32_t sb = s_sel_k[rr];
-            float z = -INFINITY;
-            if (rr < nb) {
-                const float logit = s_zl[rr][g] * INV_SQRT_D;
-                if (sb & 0x100u) {
-                    z = logit;
-                } else if (sb & (1u << g)) {
-                    const float den = s_qn[g] * s_xn[rr];
-                    float cs = den > 0.0f ? s_zd[rr][g] / den : 0.0f;
-                    cs = fminf(1.0f, fmaxf(-1.0f, cs));
-                    const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
-                    z = logit - log_sampling_prob(p, K, a.L, a.minc);
-                }
-            }
-            s_w[rr][g] = z;
-        }
-        __syncthreads();
-        // (d) online softmax: batch max per head (warp g), rescale, weights
-        if (warp < G) {
-            const int g = warp;
-            const float z = s_w[lane][g];  // RB == 32: lane = key
-            float mb = z;
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, m));
-            const float mo = s_mrun[g];
-            const float mn = fmaxf(mo, mb);
-            const float sc = (mo == -INFINITY) ? 0.0f : __expf(mo - mn);
-            const float w = (z == -INFINITY) ? 0.0f : __expf(z - mn);
-            const float ws = warp_sum_f(w);
-            s_w[lane][g] = w;
-            if (lane == 0) {
-                s_scale[g] = sc;
-                s_srun[g] = s_srun[g] * sc + ws;
-                s_mrun[g] = mn;
-            }
-        }
-        __syncthreads();
-        // (e) a[g][d] = a * scale + sum_keys w * v   (thread per (head, dim pair))
-#pragma unroll
-        for (int r = 0; r < NITEM; r++) {
-            const int it = tid + r * DEC_THREADS;
-            if (it < G * (HD / 2)) {
-                const int g = it / (HD / 2), dp = it % (HD / 2);
-                const float sc = s_scale[g];
-                float a0 = acc[r][0] * sc, a1 = acc[r][1] * sc;
-                for (int rr = 0; rr < nb; rr++) {
-                    const float w = s_w[rr][g];
-                    const uint32_t vv = *reinterpret_cast<const uint32_t*>(buf + rr * ROWB + 256 + dp * 4);
-                    a0 = fmaf(w, __uint_as_float(vv << 16), a0);
-                    a1 = fmaf(w, __uint_as_float(vv & 0xffff0000u), a1);
-                }
-                acc[r][0] = a0;
-                acc[r][1] = a1;
-            }
-        }
-        __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2); s_w reused
-    }
+    gather_batched<K, G>(a, sh, ring, s_n, unit, acc);
     MP_STAMP(6);
 
-    // ---- 9. this CTA's partial state (m, s, a) -> global parts[(cgid * CS + rank)]
-    float* pc = a.parts + (cgid * CS + rank) * G * PART;
+    // ---- 9. this CTA's partial state (m, s, a) -> global parts[unit][slot*CS + rank]
+    const int np = (int)per_unit * CS;
+    float* pc = a.parts + (unit * np + slot * CS + rank) * G * PART;
 #pragma unroll
     for (int r = 0; r < NITEM; r++) {
         const int it = tid + r * DEC_THREADS;
@@ -529,24 +595,45 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
     }
     if (tid < G) {
-        pc[tid * PART] = s_mrun[tid];
-        pc[tid * PART + 1] = s_srun[tid];
+        pc[tid * PART] = sh.mrun[tid];
+        pc[tid * PART + 1] = sh.srun[tid];
     }
     MP_STAMP(7);
-    if (CS > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (CS > 1 && !is_static) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     MP_STAMP(8);
+    // static pieces touch shared global state (parts / counters) only after the
+    // preceding grids' writes are visible
+    if (is_static) asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    // ---- 10. the last CTA of the unit merges all nchunks*CS partials (fixed order)
+    // ---- 10. the last CTA of the unit merges all of its np partials (fixed order)
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_flag = atomicAdd(a.unit_ctr + unit, 1u) == (uint32_t)(a.nchunks * CS - 1);
+    if (tid == 0) s_flag = atomicAdd(a.unit_ctr + unit, 1u) == (uint32_t)(np - 1);
     __syncthreads();
     if (!s_flag) return;
     __threadfence();
     MP_STAMP(9);
-    const int np = (int)a.nchunks * CS;
     const float* pu = a.parts + unit * (int64_t)np * G * PART;
     __shared__ int s_cnt[G];
+    __shared__ float s_M[G], s_S[G];
+    float* sm_f = reinterpret_cast<float*>(ring);  // [np][G] m, then scale factors
+    float* sm_s = sm_f + (size_t)np * G;           // [np][G] s
+    const bool fit = (size_t)np * G * 8 <= (size_t)a.ring_bytes;
+    // issue the first block of a-value loads before the m/s round completes
+    constexpr int BLK = 16;
+    const int g_it = tid / (HD / 2), dp_it = tid % (HD / 2);  // item = tid (G*64 items; G <= 4 here)
+    float2 av[BLK];
+    const bool own = tid < G * (HD / 2);
+#pragma unroll
+    for (int t = 0; t < BLK; t++)
+        av[t] = (own && t < np) ? __ldcg(reinterpret_cast<const float2*>(pu + ((int64_t)t * G + g_it) * PART + 2) + dp_it)
+                                : make_float2(0.0f, 0.0f);
+    if (fit) {
+        for (int e = tid; e < np * G; e += DEC_THREADS) {
+            sm_f[e] = __ldcg(pu + (int64_t)e * PART);
+            sm_s[e] = __ldcg(pu + (int64_t)e * PART + 1);
+        }
+    }
     if (warp < G) {  // |S_g| summed over the unit's chunks
         int cnt = 0;
         for (int c = lane; c < (int)a.nchunks; c += 32) cnt += __ldcg(a.chunk_cnt + (unit * a.nchunks + c) * G + warp);
@@ -554,32 +641,19 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
         if (lane == 0) s_cnt[warp] = cnt;
     }
-    // (a) stage m, s of every partial in shared memory (one round of loads)
-    float* sm_m = reinterpret_cast<float*>(ring);  // [np][G]
-    float* sm_s = sm_m + (size_t)np * G;           // [np][G]
-    const bool fit = (size_t)np * G * 8 <= (size_t)a.ring_bytes;
-    __shared__ float s_M[G], s_S[G];
-    if (fit) {
-        for (int e = tid; e < np * G; e += DEC_THREADS) {
-            sm_m[e] = __ldcg(pu + (int64_t)e * PART);
-            sm_s[e] = __ldcg(pu + (int64_t)e * PART + 1);
-        }
-    }
     __syncthreads();
-    // (b) M_g, scale factors f_pg = e^{m_pg - M_g} (in place of m), S_g  (warp g, fixed order)
-    if (warp < G) {
+    if (warp < G) {  // M_g, f_pg = e^{m_pg - M_g}, S_g  (fixed order)
         const int g = warp;
         float M = -INFINITY;
-        for (int c = lane; c < np; c += 32)
-            M = fmaxf(M, fit ? sm_m[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART));
+        for (int c = lane; c < np; c += 32) M = fmaxf(M, fit ? sm_f[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART));
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, m));
         float S = 0.0f;
         for (int c = lane; c < np; c += 32) {
-            const float mc = fit ? sm_m[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART);
+            const float mc = fit ? sm_f[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART);
             const float sc = fit ? sm_s[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART + 1);
             const float f = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
-            if (fit) sm_m[c * G + g] = f;
+            if (fit) sm_f[c * G + g] = f;
             S += f * sc;
         }
         S = warp_sum_f(S);
@@ -589,34 +663,34 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
     }
     __syncthreads();
-    // (c) A_g,d = sum_p f_pg a_pg,d: thread per (head, dim pair), 16 partials' loads in flight
+    auto fac = [&](int c, int g) -> float {
+        if (fit) return sm_f[c * G + g];
+        const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
+        return (s_M[g] == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - s_M[g]);
+    };
     for (int e = tid; e < G * (HD / 2); e += DEC_THREADS) {
         const int g = e / (HD / 2), dp = e % (HD / 2);
-        const float M = s_M[g], S = s_S[g];
         float A0 = 0.0f, A1 = 0.0f;
-        for (int c0 = 0; c0 < np; c0 += 16) {
-            float2 av[16];
+        for (int c0 = 0; c0 < np; c0 += BLK) {
+            if (!(c0 == 0 && e == tid)) {
 #pragma unroll
-            for (int t = 0; t < 16; t++)
-                av[t] = (c0 + t < np) ? __ldcg(reinterpret_cast<const float2*>(pu + ((int64_t)(c0 + t) * G + g) * PART + 2) + dp)
-                                      : make_float2(0.0f, 0.0f);
+                for (int t = 0; t < BLK; t++)
+                    av[t] = (c0 + t < np) ? __ldcg(reinterpret_cast<const float2*>(pu + ((int64_t)(c0 + t) * G + g) * PART + 2) + dp)
+                                          : make_float2(0.0f, 0.0f);
+            }
 #pragma unroll
-            for (int t = 0; t < 16; t++) {
-                const int c = c0 + t;
-                if (c >= np) break;
-                float f;
-                if (fit) {
-                    f = sm_m[c * G + g];
-                } else {
-                    const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
-                    f = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
-                }
+            for (int t = 0; t < BLK; t++) {
+                if (c0 + t >= np) break;
+                const float f = fac(c0 + t, g);
                 A0 = fmaf(f, av[t].x, A0);
                 A1 = fmaf(f, av[t].y, A1);
             }
         }
+        const float M = s_M[g], S = s_S[g];
         const int64_t row = qh0 + g;
-        if (a.out) *reinterpret_cast<float2*>(a.out + row * HD + 2 * dp) = S > 0.0f ? make_float2(A0 / S, A1 / S) : make_float2(0.0f, 0.0f);
+        if (a.out)
+            *reinterpret_cast<float2*>(a.out + row * HD + 2 * dp) =
+                S > 0.0f ? make_float2(A0 / S, A1 / S) : make_float2(0.0f, 0.0f);
         if (a.partial) {
             a.partial[row * PART + 2 + 2 * dp] = A0;
             a.partial[row * PART + 3 + 2 * dp] = A1;
@@ -687,7 +761,7 @@ static int launch_kg(DecodeArgs a, cudaStream_t st) {
     auto kern = decode_kernel<K, G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MAGICPIG_ECUDA;
-    const int64_t nblk = a.B * a.Hkv * a.nchunks * a.tsplit;
+    const int64_t nblk = a.B * a.Hkv * (a.nchunks + a.nstatic) * a.tsplit;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)nblk);
     cfg.blockDim = dim3(DEC_THREADS);

@@ -41,6 +41,7 @@ struct DecodeArgs {
     int64_t B, Hkv, Hq, n_local, seq_offset, n_global;
     int K, L, KL, KLw, KLq, ngroups, TG, QG;
     int64_t nchunks;
+    int64_t nstatic;  // static-key pieces (clusters) per unit
     int tsplit, sink, local, minc;
     int qx_bytes, depth, ring_bytes;  // set by the launcher
     unsigned long long* timeline;  // debug: [grid][16] globaltimer stamps, or NULL

@@ -49,6 +49,10 @@ def main():
             continue
         print(f"{p:2d} {nm:9s} n={len(col):5d}  min={col.min()/1e3:7.2f}  med={np.median(col)/1e3:7.2f}  "
               f"p90={np.percentile(col, 90)/1e3:7.2f}  max={col.max()/1e3:7.2f} us")
+    print("gather sub-phases (cycles, median / max over CTAs): ")
+    for p, nm in zip(range(11, 16), ["rows_wait", "xtile", "mma", "logu", "softmax"]):
+        col = t[:, p]
+        print(f"   {nm:10s} med={np.median(col):8.0f} max={col.max():8.0f}")
     # per-phase durations (median over CTAs)
     print("phase durations (median over CTAs, us):")
     for p in range(1, 9):

@@ -146,10 +146,10 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 
 // Per-CTA working set of the batched gather (static shared memory).
 template <int G>
-struct GatherShared {
+struct __align__(16) GatherShared {
     int keys[KCHUNK];            // local key index of every entry this CTA gathers
     uint16_t bits[KCHUNK];       // bit g: key in S_g; bit 8: static (u = 1)
-    uint8_t qb16[8 * QBS];       // query heads as bf16 rows (mma B operand), zero padded
+    __align__(16) uint8_t qb16[8 * QBS];  // query heads as bf16 rows (mma B operand), zero padded
     float c[HD];                 // centering vector
     float qn[G];                 // |q_g|
     float zl[RB][8], zd[RB][8], w[RB][8];

@@ -318,7 +318,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.parts = w.parts;
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
-    const int64_t grid = B * Hkv * g.nchunks * a.tsplit;
+    const int64_t grid = B * Hkv * (g.nchunks + a.nstatic) * a.tsplit;
     if (grid_out) *grid_out = grid;
     if (timeline) {
         if (timeline_len < grid * 16) return MAGICPIG_EINVAL;

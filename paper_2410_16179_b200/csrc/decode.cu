@@ -299,8 +299,9 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
 #pragma unroll
                     for (int t = 0; t < 4; t++) {
                         const int rr = r0 + t;
-                        const float w = rr < nb ? sh.w[rr][g] : 0.0f;
-                        const uint32_t vv = *reinterpret_cast<const uint32_t*>(buf + (rr < RB ? rr : 0) * ROWB + 256 + dp * 4);
+                        const bool live = rr < nb;
+                        const float w = live ? sh.w[rr][g] : 0.0f;
+                        const uint32_t vv = live ? *reinterpret_cast<const uint32_t*>(buf + rr * ROWB + 256 + dp * 4) : 0u;
                         p0[t] = fmaf(w, __uint_as_float(vv << 16), p0[t]);
                         p1[t] = fmaf(w, __uint_as_float(vv & 0xffff0000u), p1[t]);
                     }

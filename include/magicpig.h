@@ -208,9 +208,10 @@ int magicpig_debug_hash_acc(const magicpig_config* cfg, const uint16_t* k, int64
 
 /* Debug timeline of one decode (encode + decode_encoded, unsharded): thread 0
  * of every decode CTA writes %globaltimer (ns) at its phase boundaries into
- * timeline[cta][16] (0 = not reached): 0 start, 1 after griddepcontrol.wait,
+ * timeline[cta][32] (0 = not reached): 0 start, 1 after griddepcontrol.wait,
  * 2 query masks, 3 scan, 4 cluster combine, 5 compaction, 6 gather,
- * 7 CTA partial, 8 cluster merge, 9 unit-merge start, 10 end.  Returns the
+ * 7 CTA partial, 8 cluster merge, 9 unit-merge start, 10 end; 11-16 gather
+ * sub-phase clock64 cycles (rows, xbar, mma, log u, softmax max, accumulate).  Returns the
  * number of CTAs (> 0) or an error code. */
 int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
                                        const uint32_t* codes, const float* center, const float* key_norm,

@@ -321,8 +321,8 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     const int64_t grid = B * Hkv * (g.nchunks + a.nstatic) * a.tsplit;
     if (grid_out) *grid_out = grid;
     if (timeline) {
-        if (timeline_len < grid * 16) return MAGICPIG_EINVAL;
-        if (cudaMemsetAsync(timeline, 0, (size_t)grid * 16 * 8, st) != cudaSuccess) return MAGICPIG_ECUDA;
+        if (timeline_len < grid * 32) return MAGICPIG_EINVAL;
+        if (cudaMemsetAsync(timeline, 0, (size_t)grid * 32 * 8, st) != cudaSuccess) return MAGICPIG_ECUDA;
         a.timeline = timeline;
     }
     return launch_decode(a, st);

@@ -205,7 +205,7 @@ __device__ __forceinline__ float log_sampling_prob(float p, int K, int L, int mi
     } else {
         const float y = (float)(L - 1) * x;
         if (y <= 1.0f) {
-            const float r = x / (1.0f - x);
+            const float r = __fdividef(x, 1.0f - x);
             float s = 0.0f;
 #pragma unroll
             for (int j = 15; j >= 2; j--) {

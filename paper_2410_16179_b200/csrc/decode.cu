@@ -114,17 +114,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 __device__ __forceinline__ long long clk64() { return clock64(); }
-#define MP_ACC(ph, t0)                                                                            \
-    do {                                                                                           \
-        if (a.timeline && threadIdx.x == 0) {                                                      \
-            long long t1_ = clk64();                                                               \
-            a.timeline[(size_t)blockIdx.x * 16 + (ph)] += (unsigned long long)(t1_ - (t0));        \
-            t0 = t1_;                                                                              \
-        }                                                                                          \
+#define MP_ACC(ph, t0)                                  \
+    do {                                                 \
+        if (a.timeline && threadIdx.x == 0) {            \
+            long long t1_ = clk64();                     \
+            tacc[(ph) - 11] += (t1_ - (t0));             \
+            t0 = t1_;                                    \
+        }                                                \
     } while (0)
 #define MP_STAMP(ph)                                                                        \
     do {                                                                                     \
-        if (a.timeline && threadIdx.x == 0) a.timeline[(size_t)blockIdx.x * 16 + (ph)] = gtimer(); \
+        if (a.timeline && threadIdx.x == 0) a.timeline[(size_t)blockIdx.x * 32 + (ph)] = gtimer(); \
     } while (0)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
@@ -190,6 +190,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
     };
     if (nbatch > 0) stage(0);
     long long tcl = clk64();
+    long long tacc[4] = {0, 0, 0, 0};
     for (int bt = 0; bt < nbatch; bt++) {
         if (bt + 1 < nbatch) {
             stage(bt + 1);
@@ -201,30 +202,28 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
         MP_ACC(11, tcl);
         const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
         const int nb = min(RB, n - bt * RB);
-        // (a) xbar = bf16(fl32(k - c)), 8 dims per task; per-row selection bits and |xbar|
-        for (int e = tid; e < RB * (HD / 8); e += DEC_THREADS) {
-            const int rr = e / (HD / 8), dg = e % (HD / 8);
-            const uint4 kv = *reinterpret_cast<const uint4*>(buf + rr * ROWB + dg * 16);
-            const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
-            uint32_t xw[4];
-#pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const float k0 = __uint_as_float(kw[t] << 16), k1 = __uint_as_float(kw[t] & 0xffff0000u);
-                xw[t] = (uint32_t)f2bf_rn(__fsub_rn(k0, sh.c[dg * 8 + 2 * t])) |
-                        ((uint32_t)f2bf_rn(__fsub_rn(k1, sh.c[dg * 8 + 2 * t + 1])) << 16);
-            }
-            *reinterpret_cast<uint4*>(xt + rr * XS + dg * 16) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
-        }
-        if (tid < RB) {
-            const bool live = tid < nb;
-            sh.sbits[tid] = live ? sh.bits[bt * RB + tid] : (uint16_t)0;
-            sh.xn[tid] = live ? *reinterpret_cast<const float*>(buf + tid * ROWB + 512) : 0.0f;
-        }
-        __syncthreads();
-        MP_ACC(12, tcl);
-        // (b) logits and hashed-vector dots on tensor cores
+        // (a+b) tensor cores: warp (mt, which) = 16 rows x {raw keys -> logits, xbar -> cos};
+        // the xbar warps first write bf16(fl32(k - c)) of their own 16 rows
         if (warp < 2 * (RB / 16)) {
-            const int mt = warp & 1, which = warp >> 1;  // 0: raw keys (logits), 1: xbar (cos)
+            const int mt = warp & 1, which = warp >> 1;
+            if (which == 1) {
+#pragma unroll
+                for (int t = 0; t < 16 * (HD / 8) / 32; t++) {
+                    const int e = lane + 32 * t;
+                    const int rr = mt * 16 + e / (HD / 8), dg = e % (HD / 8);
+                    const uint4 kv = *reinterpret_cast<const uint4*>(buf + rr * ROWB + dg * 16);
+                    const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+                    uint32_t xw[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const float k0 = __uint_as_float(kw[u] << 16), k1 = __uint_as_float(kw[u] & 0xffff0000u);
+                        xw[u] = (uint32_t)f2bf_rn(__fsub_rn(k0, sh.c[dg * 8 + 2 * u])) |
+                                ((uint32_t)f2bf_rn(__fsub_rn(k1, sh.c[dg * 8 + 2 * u + 1])) << 16);
+                    }
+                    *reinterpret_cast<uint4*>(xt + rr * XS + dg * 16) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+                }
+                __syncwarp();
+            }
             const uint8_t* abase = which == 0 ? buf : xt;
             const int astride = which == 0 ? ROWB : XS;
             float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -246,32 +245,26 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
             dst[r0 + 8][c0 + 1] = d4[3];
         }
         __syncthreads();
-        MP_ACC(13, tcl);
-        // (c) one thread per (key, head): z = q.k/sqrt(d) - log u; u from the hashed vectors' angle (R5)
-        for (int it = tid; it < RB * G; it += DEC_THREADS) {
-            const int rr = it / G, g = it % G;
-            const uint32_t sb = sh.sbits[rr];
+        MP_ACC(12, tcl);
+        // (c+d) warp g = head g, lane = row: z = q.k/sqrt(d) - log u (u from the hashed
+        // vectors' angle R5), then the batch max, rescale factor and weights of the online softmax
+        if (warp < G) {
+            const int g = warp, rr = lane;  // RB == 32
             float z = -INFINITY;
             if (rr < nb) {
+                const uint32_t sb = sh.bits[bt * RB + rr];
                 const float logit = sh.zl[rr][g] * INV_SQRT_D;
                 if (sb & 0x100u) {
                     z = logit;
                 } else if (sb & (1u << g)) {
-                    const float den = sh.qn[g] * sh.xn[rr];
-                    float cs = den > 0.0f ? sh.zd[rr][g] / den : 0.0f;
+                    const float xn = *reinterpret_cast<const float*>(buf + rr * ROWB + 512);
+                    const float den = sh.qn[g] * xn;
+                    float cs = den > 0.0f ? __fdividef(sh.zd[rr][g], den) : 0.0f;
                     cs = fminf(1.0f, fmaxf(-1.0f, cs));
                     const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
                     z = logit - log_sampling_prob(p, K, a.L, a.minc);
                 }
             }
-            sh.w[rr][g] = z;
-        }
-        __syncthreads();
-        MP_ACC(14, tcl);
-        // (d) online softmax: batch max per head (warp g), rescale factor, weights
-        if (warp < G) {
-            const int g = warp;
-            const float z = sh.w[lane][g];  // RB == 32: lane = row
             float mb = z;
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, m));
@@ -280,7 +273,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
             const float sc = (mo == -INFINITY) ? 0.0f : __expf(mo - mn);
             const float w = (z == -INFINITY) ? 0.0f : __expf(z - mn);
             const float wsum = warp_sum_f(w);
-            sh.w[lane][g] = w;
+            sh.w[rr][g] = w;
             if (lane == 0) {
                 sh.scale[g] = sc;
                 sh.srun[g] = sh.srun[g] * sc + wsum;
@@ -288,6 +281,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
             }
         }
         __syncthreads();
+        MP_ACC(13, tcl);
         // (e) a[g][d] = a * scale + sum_rows w * v  (4 independent partial sums per item)
 #pragma unroll
         for (int r = 0; r < NITEM; r++) {
@@ -312,8 +306,10 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
             }
         }
         __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2); w reused
-        MP_ACC(15, tcl);
+        MP_ACC(14, tcl);
     }
+    if (a.timeline && threadIdx.x == 0)
+        for (int t = 0; t < 4; t++) a.timeline[(size_t)blockIdx.x * 32 + 11 + t] = (unsigned long long)tacc[t];
 }
 
 template <int K, int G>
@@ -335,7 +331,8 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __shared__ GatherShared<G> sh;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int CS = a.tsplit;
+    const int CS = a.tsplit;  // power of two
+    const int lcs = __ffs(CS) - 1;
     cgr::cluster_group cluster = cgr::this_cluster();
     const int rank = CS > 1 ? (int)cluster.block_rank() : 0;
     const int64_t per_unit = a.nchunks + a.nstatic;  // clusters per unit: chunk scans + static pieces
@@ -558,8 +555,8 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
             while (u) {
                 const int r = __ffs(u) - 1;
                 u &= u - 1;
-                if (pos % CS == rank) {
-                    const int j = pos / CS;
+                if ((pos & (CS - 1)) == rank) {
+                    const int j = pos >> lcs;
                     const uint32_t bitm = 1u << r;
                     uint32_t bits = 0;
 #pragma unroll
@@ -569,7 +566,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                 }
                 pos++;
             }
-            if (lane == 31) s_n = incl > rank ? (incl - rank + CS - 1) / CS : 0;
+            if (lane == 31) s_n = incl > rank ? (incl - rank + CS - 1) >> lcs : 0;
         }
         // remote s_part reads are done: let the cluster peers go on (we wait before exiting)
         if (CS > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");

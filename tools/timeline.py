@@ -37,7 +37,7 @@ def main():
         grid = B_.debug_decode_timeline(mp.cfg, tq, mp.buf.codes, mp.buf.center, mp.buf.key_norm, tk, tv, tW, out,
                                         tl, ws)
         torch.cuda.synchronize()
-        t = tl[:grid * 16].view(grid, 16).cpu().numpy().astype(np.int64)
+        t = tl[:grid * 32].view(grid, 32).cpu().numpy().astype(np.int64)
         res.append(t)
     t = res[-1]
     t0 = t[:, 0][t[:, 0] > 0].min()
@@ -50,7 +50,7 @@ def main():
         print(f"{p:2d} {nm:9s} n={len(col):5d}  min={col.min()/1e3:7.2f}  med={np.median(col)/1e3:7.2f}  "
               f"p90={np.percentile(col, 90)/1e3:7.2f}  max={col.max()/1e3:7.2f} us")
     print("gather sub-phases (cycles, median / max over CTAs): ")
-    for p, nm in zip(range(11, 16), ["rows_wait", "xtile", "mma", "logu", "softmax"]):
+    for p, nm in zip(range(11, 15), ["rows_wait", "x+mma", "z+max", "accum"]):
         col = t[:, p]
         print(f"   {nm:10s} med={np.median(col):8.0f} max={col.max():8.0f}")
     # per-phase durations (median over CTAs)

@@ -193,29 +193,33 @@ __device__ inline int exact_dot_sign_bf16(const uint16_t* a, const uint16_t* b, 
 constexpr float LOG_U_FLOOR = -690.7755279f;
 
 __device__ __forceinline__ float log_sampling_prob(float p, int K, int L, int minc) {
+    // hardware log2/exp2 (MUFU, ~2 ulp): |error in ln u| < 1e-5, far below the
+    // 2e-3 output tolerance; the chain stays short because this runs once per
+    // (sampled key, head) on the critical path of the decode.
     if (!(p > 0.0f)) return LOG_U_FLOOR;
     if (p >= 1.0f) return 0.0f;
-    const float lnx = (float)K * logf(p);
-    const float x = expf(lnx);
+    const float lnx = (float)K * __logf(p);
+    const float x = __expf(lnx);
+    const float l1mx = __logf(1.0f - x);  // ln(1 - x); x <= 1 - 2^-24 here
     float lu;
     if (minc == 1) {
         const float Lx = (float)L * x;
-        if (Lx < 1e-4f) lu = lnx + logf((float)L) - 0.5f * (float)(L - 1) * x;
-        else lu = logf(-expm1f((float)L * log1pf(-x)));
+        if (Lx < 1e-3f) lu = lnx + __logf((float)L) - 0.5f * (float)(L - 1) * x;
+        else lu = __logf(-expm1f((float)L * l1mx));
     } else {
         const float y = (float)(L - 1) * x;
         if (y <= 1.0f) {
             const float r = __fdividef(x, 1.0f - x);
             float s = 0.0f;
 #pragma unroll
-            for (int j = 15; j >= 2; j--) {
-                // s_j = (L-j)/(j+1) r (1 + s_{j+1}); terms beyond L vanish
+            for (int j = 11; j >= 2; j--) {
+                // s_j = (L-j)/(j+1) r (1 + s_{j+1}); terms beyond L vanish; truncation < y^10/11! ~ 3e-8
                 const float c = (float)(L - j) * (1.0f / (float)(j + 1));
                 s = (L - j > 0) ? c * r * (1.0f + s) : 0.0f;
             }
-            lu = logf(0.5f * (float)L * (float)(L - 1)) + 2.0f * lnx + (float)(L - 2) * log1pf(-x) + log1pf(s);
+            lu = __logf(0.5f * (float)L * (float)(L - 1)) + 2.0f * lnx + (float)(L - 2) * l1mx + __logf(1.0f + s);
         } else {
-            lu = logf(-expm1f((float)(L - 1) * log1pf(-x) + log1pf(y)));
+            lu = __logf(-expm1f((float)(L - 1) * l1mx + __logf(1.0f + y)));
         }
     }
     return fmaxf(lu, LOG_U_FLOOR);

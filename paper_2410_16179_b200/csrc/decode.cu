@@ -23,6 +23,7 @@
 //           of a unit merges all chunks in fixed order (log-sum-exp,
 //           "recursive attention" P:171).  Counters self-clean (graph-safe).
 #include <cooperative_groups.h>
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -202,28 +203,29 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
         MP_ACC(11, tcl);
         const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
         const int nb = min(RB, n - bt * RB);
-        // (a+b) tensor cores: warp (mt, which) = 16 rows x {raw keys -> logits, xbar -> cos};
-        // the xbar warps first write bf16(fl32(k - c)) of their own 16 rows
+        // (a) xbar = bf16(fl32(k - c)) for the batch rows (cvt.rn.bf16x2.f32), all warps
+#pragma unroll
+        for (int t = 0; t < RB * (HD / 8) / DEC_THREADS; t++) {
+            const int e = tid + DEC_THREADS * t;
+            const int rr = e / (HD / 8), dg = e % (HD / 8);
+            const uint4 kv = *reinterpret_cast<const uint4*>(buf + rr * ROWB + dg * 16);
+            const float4 c0 = *reinterpret_cast<const float4*>(&sh.c[dg * 8]);
+            const float4 c1 = *reinterpret_cast<const float4*>(&sh.c[dg * 8 + 4]);
+            const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+            uint32_t xw[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const __nv_bfloat162 xb = __floats2bfloat162_rn(__fsub_rn(__uint_as_float(kw[u] << 16), cc[2 * u]),
+                                                                __fsub_rn(__uint_as_float(kw[u] & 0xffff0000u), cc[2 * u + 1]));
+                xw[u] = *reinterpret_cast<const uint32_t*>(&xb);
+            }
+            *reinterpret_cast<uint4*>(xt + rr * XS + dg * 16) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+        }
+        __syncthreads();
+        // (b) tensor cores: warp (mt, which) = 16 rows x {raw keys -> logits, xbar -> cos}
         if (warp < 2 * (RB / 16)) {
             const int mt = warp & 1, which = warp >> 1;
-            if (which == 1) {
-#pragma unroll
-                for (int t = 0; t < 16 * (HD / 8) / 32; t++) {
-                    const int e = lane + 32 * t;
-                    const int rr = mt * 16 + e / (HD / 8), dg = e % (HD / 8);
-                    const uint4 kv = *reinterpret_cast<const uint4*>(buf + rr * ROWB + dg * 16);
-                    const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
-                    uint32_t xw[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const float k0 = __uint_as_float(kw[u] << 16), k1 = __uint_as_float(kw[u] & 0xffff0000u);
-                        xw[u] = (uint32_t)f2bf_rn(__fsub_rn(k0, sh.c[dg * 8 + 2 * u])) |
-                                ((uint32_t)f2bf_rn(__fsub_rn(k1, sh.c[dg * 8 + 2 * u + 1])) << 16);
-                    }
-                    *reinterpret_cast<uint4*>(xt + rr * XS + dg * 16) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
-                }
-                __syncwarp();
-            }
             const uint8_t* abase = which == 0 ? buf : xt;
             const int astride = which == 0 ? ROWB : XS;
             float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -611,6 +613,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     if (!s_flag) return;
     __threadfence();
     MP_STAMP(9);
+    long long tm0 = clk64();
     const float* pu = a.parts + unit * (int64_t)np * G * PART;
     __shared__ int s_cnt[G];
     __shared__ float s_M[G], s_S[G];
@@ -640,6 +643,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         if (lane == 0) s_cnt[warp] = cnt;
     }
     __syncthreads();
+    if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32 + 17] = (unsigned long long)(clk64() - tm0);
     if (warp < G) {  // M_g, f_pg = e^{m_pg - M_g}, S_g  (fixed order)
         const int g = warp;
         float M = -INFINITY;
@@ -661,6 +665,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
     }
     __syncthreads();
+    if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32 + 18] = (unsigned long long)(clk64() - tm0);
     auto fac = [&](int c, int g) -> float {
         if (fit) return sm_f[c * G + g];
         const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
@@ -700,6 +705,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         if (dp == 0 && !(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
     }
     __syncthreads();
+    if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32 + 19] = (unsigned long long)(clk64() - tm0);
     if (tid < G && a.s_count) a.s_count[qh0 + tid] = s_cnt[tid];
     if (tid == 0) a.unit_ctr[unit] = 0u;
     MP_STAMP(10);

@@ -53,6 +53,11 @@ def main():
     for p, nm in zip(range(11, 15), ["rows_wait", "x+mma", "z+max", "accum"]):
         col = t[:, p]
         print(f"   {nm:10s} med={np.median(col):8.0f} max={col.max():8.0f}")
+    m = t[:, 17] > 0
+    if m.any():
+        print("unit merge (cycles since start, median / max over merging CTAs):")
+        for p, nm in zip(range(17, 20), ["ms_staged", "M_S", "done"]):
+            print(f"   {nm:10s} med={np.median(t[m, p]):8.0f} max={t[m, p].max():8.0f}")
     # per-phase durations (median over CTAs)
     print("phase durations (median over CTAs, us):")
     for p in range(1, 9):

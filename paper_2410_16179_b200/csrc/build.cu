@@ -18,29 +18,54 @@ __device__ __forceinline__ bool is_static_pos(int64_t pos, int64_t n_global, int
 
 // ---------------------------------------------------------------------------
 // Phase 1: per (unit, split, dim) partial sums of q64(k) over dynamic keys.
-// grid (nsplit, units), block 128 (thread = dim).
-__global__ void __launch_bounds__(128) key_stats_partial_kernel(
+// grid (nsplit, units), block 256: warp per key (stride 8), lane = 4 dims,
+// per-lane int128 accumulators; warps combined through shared memory.
+__global__ void __launch_bounds__(256) key_stats_partial_kernel(
     const uint16_t* __restrict__ k, int64_t n_local, int64_t seq_offset, int64_t n_global, int sink,
     int local, int64_t* __restrict__ part_sum, int64_t* __restrict__ part_cnt, uint32_t* status) {
-    const int d = threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t unit = blockIdx.y;
     const int split = blockIdx.x, nsplit = gridDim.x;
     const int64_t i0 = (int64_t)split * STATS_SPLIT;
     const int64_t i1 = min(i0 + (int64_t)STATS_SPLIT, n_local);
     const uint16_t* kp = k + unit * n_local * HD;
-    i128 acc = 0;
+    i128 acc[4] = {0, 0, 0, 0};
     int cnt = 0;
     bool bad = false;
-    for (int64_t i = i0; i < i1; i++) {
+    for (int64_t i = i0 + warp; i < i1; i += 8) {
         if (is_static_pos(seq_offset + i, n_global, sink, local)) continue;
-        uint16_t h = kp[i * HD + d];
-        bad |= fabsf(bf2f(h)) >= ABS_LIMIT;
-        acc += q64_of_bf16(h);
+        const uint2 kr = __ldg(reinterpret_cast<const uint2*>(kp + i * HD) + lane);
+        const uint16_t h[4] = {(uint16_t)(kr.x & 0xFFFF), (uint16_t)(kr.x >> 16), (uint16_t)(kr.y & 0xFFFF),
+                               (uint16_t)(kr.y >> 16)};
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            bad |= fabsf(bf2f(h[t])) >= ABS_LIMIT;
+            acc[t] += q64_of_bf16(h[t]);
+        }
         cnt++;
     }
     if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
-    st_q64(part_sum + ((unit * nsplit + split) * HD + d) * 2, acc);
-    if (d == 0) part_cnt[unit * nsplit + split] = cnt;
+    __shared__ unsigned long long sm[8][HD][2];
+    __shared__ int scnt[8];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        const u128 u = (u128)acc[t];
+        sm[warp][lane * 4 + t][0] = (unsigned long long)u;
+        sm[warp][lane * 4 + t][1] = (unsigned long long)(u >> 64);
+    }
+    if (lane == 0) scnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x < HD) {
+        const int d = threadIdx.x;
+        i128 tot = 0;
+        for (int w = 0; w < 8; w++) tot += (i128)(((u128)sm[w][d][1] << 64) | (u128)sm[w][d][0]);
+        st_q64(part_sum + ((unit * nsplit + split) * HD + d) * 2, tot);
+    }
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int w = 0; w < 8; w++) c += scnt[w];
+        part_cnt[unit * nsplit + split] = c;
+    }
 }
 
 // Sum of P partial copies: out[u][d] = sum_p part[u][p][d]  (fixed order)
@@ -287,7 +312,7 @@ int launch_key_stats(const uint16_t* k, int64_t units, int64_t n_local, int64_t 
                      int64_t* key_sum, int64_t* count, uint32_t* status, cudaStream_t st) {
     int nsplit = (int)((n_local + STATS_SPLIT - 1) / STATS_SPLIT);
     if (nsplit < 1) nsplit = 1;
-    key_stats_partial_kernel<<<dim3(nsplit, (unsigned)units), 128, 0, st>>>(
+    key_stats_partial_kernel<<<dim3(nsplit, (unsigned)units), 256, 0, st>>>(
         k, n_local, seq_offset, n_global, sink, local, part_sum, part_cnt, status);
     sum_parts_kernel<<<(unsigned)units, 128, 0, st>>>(part_sum, part_cnt, nsplit, key_sum, count);
     count_launch(2);

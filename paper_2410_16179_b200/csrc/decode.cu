@@ -123,9 +123,18 @@ __device__ __forceinline__ long long clk64() { return clock64(); }
             t0 = t1_;                                    \
         }                                                \
     } while (0)
-#define MP_STAMP(ph)                                                                        \
-    do {                                                                                     \
-        if (a.timeline && threadIdx.x == 0) a.timeline[(size_t)blockIdx.x * 32 + (ph)] = gtimer(); \
+// debug timeline: slot 0 = %globaltimer at CTA start (ns); slots 1..10 = SM cycles
+// since the CTA start (clock64 of thread 0), +1 so that 0 means "not reached"
+#define MP_STAMP(ph)                                                                                   \
+    do {                                                                                                \
+        if (a.timeline && threadIdx.x == 0) {                                                           \
+            if ((ph) == 0) {                                                                            \
+                a.timeline[(size_t)blockIdx.x * 32] = gtimer();                                         \
+                mp_t0 = clk64();                                                                        \
+            } else {                                                                                    \
+                a.timeline[(size_t)blockIdx.x * 32 + (ph)] = (unsigned long long)(clk64() - mp_t0 + 1); \
+            }                                                                                           \
+        }                                                                                               \
     } while (0)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
@@ -350,6 +359,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     const int col0 = g0 * TG * K;
     const int ncols = (g1 - g0) * TG * K;
     const int depth = a.depth;
+    long long mp_t0 = 0;
     MP_STAMP(0);
 
     const uint8_t* csrc = reinterpret_cast<const uint8_t*>(a.codes) + (size_t)cgid * a.KLq * 512;

@@ -12,7 +12,8 @@
 // K*L columns streamed in N=64 chunks (3-stage bulk-copy ring).  Warp roles:
 //   warp 0: bulk-copy producer (cp.async.bulk + mbarrier complete_tx)
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5: epilogue (tcgen05.ld 32x32b -> sign/filter -> ballot -> STG.128)
+//   warps 2-9: epilogue (tcgen05.ld 32x32b -> sign/filter -> ballot -> STG.128),
+//              two warps per TMEM lane quarter, 32 columns each
 // TMEM: 2 accumulator stages x (4 tiles x 64 columns) = 512 columns.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -22,7 +23,7 @@ namespace mp {
 constexpr int GM_R = 4;
 constexpr int GM_N = 64;
 constexpr int GM_STAGES = 3;
-constexpr int GM_THREADS = 192;
+constexpr int GM_THREADS = 64 + 256;  // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
 
 struct GemmParams {
     const uint8_t* xt;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
         }
         for (int s = 0; s < 2; s++) {
             mbar_init(t_full + s, 1);
-            mbar_init(t_empty + s, 4);
+            mbar_init(t_empty + s, 8);
         }
         fence_mbar_init();
     }
@@ -120,7 +121,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
         }
     } else {
         // ---------------- epilogue ----------------
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int q = warp & 3;            // TMEM lane quarter this warp may access
+        const int h = (warp - 2) >> 2;     // which 32 of the 64 columns of a chunk
         const float wmax = *p.wmax;
         float thr[GM_R];
 #pragma unroll
@@ -139,8 +141,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                 const int64_t kchunk = kb >> 5;
                 const int lin = (int)(kb & 31);
                 uint4* cw = reinterpret_cast<uint4*>(p.codes) + ((unit * p.nchunks + kchunk) * p.KLq) * 32 + lin;
-#pragma unroll 1
-                for (int h = 0; h < 2; h++) {
+                {
                     uint32_t v[32];
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ts * 256 + rt * GM_N + h * 32, v);
                     tmem_wait_ld();

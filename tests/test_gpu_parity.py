@@ -196,7 +196,7 @@ def test_g1_golden_padded_to_d128():
 
 
 def test_tensor_core_accumulation_error_bound():
-    """The fix-up filter threshold eps = 2^-15 must dominate the tcgen05 fp32
+    """The fix-up filter threshold eps = 2^-19 must dominate the tcgen05 fp32
     accumulation error: measure max |acc - exact| / (|xbar| |W_j|)."""
     pkg = _pkg()
     wl = synth.Workload("acc", 803, B=1, Hq=1, Hkv=1, n=128, K=10, L=150)
@@ -217,7 +217,7 @@ def test_tensor_core_accumulation_error_bound():
     rel = np.abs(acc.cpu().numpy().astype(np.float64) - exact) / np.maximum(scale, 1e-30)
     worst = float(rel.max())
     print(f"tcgen05 bf16 accumulation: max |acc-exact|/(|x||w|) = {worst:.3e} (2^{np.log2(max(worst, 1e-300)):.1f})")
-    assert worst < 2.0 ** -18, worst
+    assert worst < 2.0 ** -22, worst  # eps / 8
 
 
 def test_sequence_sharding_emulated():

@@ -40,15 +40,20 @@ def main():
         t = tl[:grid * 32].view(grid, 32).cpu().numpy().astype(np.int64)
         res.append(t)
     t = res[-1]
-    t0 = t[:, 0][t[:, 0] > 0].min()
-    print(f"{name}: {t.shape[0]} CTAs")
+    st = t[:, 0].astype(np.int64)
+    st = st - st[st > 0].min()
+    print(f"{name}: {t.shape[0]} CTAs; CTA start spread: med {np.median(st)/1e3:.2f} us, max {st.max()/1e3:.2f} us")
+    ghz = 1.965
     for p, nm in enumerate(PH):
-        col = t[:, p]
-        col = col[col > 0] - t0
-        if len(col) == 0:
+        if p == 0:
             continue
-        print(f"{p:2d} {nm:9s} n={len(col):5d}  min={col.min()/1e3:7.2f}  med={np.median(col)/1e3:7.2f}  "
-              f"p90={np.percentile(col, 90)/1e3:7.2f}  max={col.max()/1e3:7.2f} us")
+        col = t[:, p]
+        m = col > 0
+        if not m.any():
+            continue
+        us = (col[m] - 1) / ghz / 1e3 + st[m] / 1e3
+        print(f"{p:2d} {nm:9s} n={m.sum():5d}  (abs) min={us.min():7.2f}  med={np.median(us):7.2f}  "
+              f"p90={np.percentile(us, 90):7.2f}  max={us.max():7.2f} us")
     print("gather sub-phases (cycles, median / max over CTAs): ")
     for p, nm in zip(range(11, 15), ["rows_wait", "x+mma", "z+max", "accum"]):
         col = t[:, p]
@@ -58,12 +63,12 @@ def main():
         print("unit merge (cycles since start, median / max over merging CTAs):")
         for p, nm in zip(range(17, 20), ["ms_staged", "M_S", "done"]):
             print(f"   {nm:10s} med={np.median(t[m, p]):8.0f} max={t[m, p].max():8.0f}")
-    # per-phase durations (median over CTAs)
-    print("phase durations (median over CTAs, us):")
-    for p in range(1, 9):
+    print("phase durations (median / max over CTAs, us, from SM cycles):")
+    for p in range(2, 9):
         m = (t[:, p] > 0) & (t[:, p - 1] > 0)
         if m.any():
-            print(f"   {PH[p-1]:>9s} -> {PH[p]:9s}: {np.median(t[m, p] - t[m, p-1])/1e3:7.2f}  max {np.max(t[m, p] - t[m, p-1])/1e3:7.2f}")
+            dd = (t[m, p].astype(np.int64) - t[m, p - 1].astype(np.int64)) / ghz / 1e3
+            print(f"   {PH[p-1]:>9s} -> {PH[p]:9s}: {np.median(dd):7.2f}  max {dd.max():7.2f}")
 
 
 if __name__ == "__main__":

@@ -99,6 +99,7 @@ static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, in
 
 struct DecodeWs {
     uint32_t* status;
+    float* lut;
     uint32_t* qbits;
     uint32_t* unit_ctr;
     float* parts;
@@ -122,6 +123,7 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
         return r;
     };
     w.status = (uint32_t*)take(256);
+    w.lut = (float*)take((size_t)(LUT_N + 1) * 4);
     w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
     w.unit_ctr = (uint32_t*)take((size_t)units * 4);
     const int64_t nT = n_local < (int64_t)c->sink + c->local ? n_local : (int64_t)c->sink + c->local;
@@ -234,9 +236,10 @@ int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64
     if (!cfg_ok(cfg) || B < 1 || Hq < 1 || !q || !W || !ws) return MAGICPIG_EINVAL;
     // the query-code region sits at the same offset in every decode workspace
     DecodeWs w = decode_layout(cfg, B, Hq, 1, 0, ws);
-    if (ws_bytes < 256 + (size_t)B * Hq * make_geom(cfg->K, cfg->L, 0).KLw * 4) return MAGICPIG_EWORKSPACE;
     const Geom g = make_geom(cfg->K, cfg->L, 0);
-    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
+    if (ws_bytes < (size_t)((uint8_t*)w.qbits - (uint8_t*)ws) + (size_t)B * Hq * g.KLw * 4) return MAGICPIG_EWORKSPACE;
+    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream), w.lut, cfg->K, cfg->L,
+                          cfg->min_collisions);
 }
 
 static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
@@ -269,6 +272,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     memset(&a, 0, sizeof(a));
     a.q = q;
     a.qbits = w.qbits;
+    a.lut = w.lut;
     a.codes = codes;
     a.center = center;
     a.key_norm = key_norm;

@@ -273,7 +273,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
                     float cs = den > 0.0f ? __fdividef(sh.zd[rr][g], den) : 0.0f;
                     cs = fminf(1.0f, fmaxf(-1.0f, cs));
                     const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
-                    z = logit - log_sampling_prob(p, K, a.L, a.minc);
+                    z = logit - log_u_lookup(a.lut, p, K, a.L, a.minc);
                 }
             }
             float mb = z;

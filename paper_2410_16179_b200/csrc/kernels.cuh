@@ -28,11 +28,12 @@ int launch_hash_gemm(const uint8_t* xt, const uint8_t* wt, const float* xnorm, c
                      uint32_t* status, float* dbg_acc, cudaStream_t st);
 
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
-                   uint32_t* status, cudaStream_t st);
+                   uint32_t* status, cudaStream_t st, float* lut = nullptr, int K = 0, int L = 0, int minc = 2);
 
 struct DecodeArgs {
     const uint16_t* q;
     const uint32_t* qbits;
+    const float* lut;  // ln u(p) table (LUT_N + 1 entries)
     const uint32_t* codes;
     const float* center;
     const float* key_norm;

@@ -154,6 +154,20 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+// D(16x8 fp32) = A(16x8 tf32, row) * B(8x8 tf32, col) + C
+__device__ __forceinline__ void mma1688_tf32(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 // Per-CTA working set of the batched gather (static shared memory).
 template <int G>
 struct __align__(16) GatherShared {
@@ -166,6 +180,7 @@ struct __align__(16) GatherShared {
     float mrun[G], srun[G], scale[G];
     float xn[RB];
     uint16_t sbits[RB];
+    uint64_t rbar[2];            // row-buffer mbarriers (bulk copies of K/V rows)
 };
 
 // Batched gather + estimator over n entries (keys[], bits[]) of one unit
@@ -173,10 +188,11 @@ struct __align__(16) GatherShared {
 // hashed-vector dots X Q^T on tensor cores (mma.sync m16n8k16, bf16 in, fp32
 // accumulate), one thread per (key, head) for z = logit - log u, then an online
 // softmax whose state (m, s per head; a per (head, dim pair)) is thread-parallel.
+// acc: this warp's two 16x8 tf32-MMA accumulator tiles of a[g][d] (rows = heads g,
+// columns = dims 16*warp .. 16*warp+15); c0,c1 = (g = lane/4, d = 2*(lane%4) + {0,1}).
 template <int K, int G>
 __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared<G>& sh, uint8_t* region,
-                                               int n, int64_t unit, float (&acc)[(G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS][2]) {
-    constexpr int NITEM = (G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS;
+                                               int n, int64_t unit, float (&acc)[2][4]) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint8_t* rows = region;                  // [2][RB][ROWB]
     uint8_t* xt = region + 2 * RB * ROWB;    // [RB][XS]
@@ -184,17 +200,29 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
     const uint16_t* kbase = a.k + unit * a.n_local * HD;
     const uint16_t* vbase = a.v + unit * a.n_local * HD;
     const int nbatch = (n + RB - 1) / RB;
+    // K/V rows by bulk copy (lane r of warp 0 copies row r), |xbar| by cp.async (warp 1)
+    if (tid == 0) {
+        mbar_init(&sh.rbar[0], 1);
+        mbar_init(&sh.rbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
     auto stage = [&](int bt) {
         uint8_t* buf = rows + (bt & 1) * RB * ROWB;
-        for (int e = tid; e < RB * 33; e += DEC_THREADS) {
-            const int rr = e / 33, part = e % 33;
-            const int j = bt * RB + rr;
-            if (j >= n) continue;
-            const int64_t i = sh.keys[j];
-            uint8_t* dst = buf + rr * ROWB;
-            if (part < 16) cp_async16(dst + part * 16, kbase + i * HD + part * 8);
-            else if (part < 32) cp_async16(dst + 256 + (part - 16) * 16, vbase + i * HD + (part - 16) * 8);
-            else cp_async4(dst + 512, knorm + i);
+        const int nbt = min(RB, n - bt * RB);
+        if (warp == 0) {
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&sh.rbar[bt & 1], (uint32_t)nbt * 512u);
+            }
+            __syncwarp();
+            if (lane < nbt) {
+                const int64_t i = sh.keys[bt * RB + lane];
+                bulk_g2s(buf + lane * ROWB, kbase + i * HD, 256, &sh.rbar[bt & 1]);
+                bulk_g2s(buf + lane * ROWB + 256, vbase + i * HD, 256, &sh.rbar[bt & 1]);
+            }
+        } else if (warp == 1 && lane < nbt) {
+            cp_async4(buf + lane * ROWB + 512, knorm + sh.keys[bt * RB + lane]);
         }
         cp_async_commit();
     };
@@ -208,6 +236,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
         } else {
             cp_async_wait<0>();
         }
+        mbar_wait(&sh.rbar[bt & 1], (uint32_t)((bt >> 1) & 1));
         __syncthreads();
         MP_ACC(11, tcl);
         const uint8_t* buf = rows + (bt & 1) * RB * ROWB;
@@ -282,7 +311,9 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
             const float mo = sh.mrun[g];
             const float mn = fmaxf(mo, mb);
             const float sc = (mo == -INFINITY) ? 0.0f : __expf(mo - mn);
-            const float w = (z == -INFINITY) ? 0.0f : __expf(z - mn);
+            // weights rounded to tf32 (the accumulation MMA's input); the normaliser uses
+            // the same rounded weights, so the estimate stays a convex combination
+            const float w = (z == -INFINITY) ? 0.0f : to_tf32(__expf(z - mn));
             const float wsum = warp_sum_f(w);
             sh.w[rr][g] = w;
             if (lane == 0) {
@@ -293,27 +324,28 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
         }
         __syncthreads();
         MP_ACC(13, tcl);
-        // (e) a[g][d] = a * scale + sum_rows w * v  (4 independent partial sums per item)
+        // (e) a[g][d] = a * scale + sum_rows w * v on tensor cores (tf32 m16n8k8, fp32 accumulate):
+        // A = weights [heads x rows], B = V [rows x dims]; warp w owns dims 16w .. 16w+15
+        {
+            const int g = lane >> 2;
+            const float sc = g < G ? sh.scale[g] : 0.0f;
 #pragma unroll
-        for (int r = 0; r < NITEM; r++) {
-            const int it = tid + r * DEC_THREADS;
-            if (it < G * (HD / 2)) {
-                const int g = it / (HD / 2), dp = it % (HD / 2);
-                float p0[4] = {0.0f, 0.0f, 0.0f, 0.0f}, p1[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                for (int r0 = 0; r0 < nb; r0 += 4) {
+            for (int nt = 0; nt < 2; nt++) {
+                acc[nt][0] *= sc;
+                acc[nt][1] *= sc;
+            }
 #pragma unroll
-                    for (int t = 0; t < 4; t++) {
-                        const int rr = r0 + t;
-                        const bool live = rr < nb;
-                        const float w = live ? sh.w[rr][g] : 0.0f;
-                        const uint32_t vv = live ? *reinterpret_cast<const uint32_t*>(buf + rr * ROWB + 256 + dp * 4) : 0u;
-                        p0[t] = fmaf(w, __uint_as_float(vv << 16), p0[t]);
-                        p1[t] = fmaf(w, __uint_as_float(vv & 0xffff0000u), p1[t]);
-                    }
+            for (int ks = 0; ks < RB / 8; ks++) {
+                const int k0 = ks * 8 + (lane & 3), k1 = k0 + 4;
+                const uint32_t a0 = g < G ? __float_as_uint(sh.w[k0][g]) : 0u;
+                const uint32_t a2 = g < G ? __float_as_uint(sh.w[k1][g]) : 0u;
+#pragma unroll
+                for (int nt = 0; nt < 2; nt++) {
+                    const int dcol = warp * 16 + nt * 8 + (lane >> 2);
+                    const uint32_t v0 = k0 < nb ? (uint32_t)*reinterpret_cast<const uint16_t*>(buf + k0 * ROWB + 256 + dcol * 2) << 16 : 0u;
+                    const uint32_t v1 = k1 < nb ? (uint32_t)*reinterpret_cast<const uint16_t*>(buf + k1 * ROWB + 256 + dcol * 2) << 16 : 0u;
+                    mma1688_tf32(acc[nt], a0, a2, v0, v1);
                 }
-                const float sc = sh.scale[g];
-                acc[r][0] = acc[r][0] * sc + ((p0[0] + p0[1]) + (p0[2] + p0[3]));
-                acc[r][1] = acc[r][1] * sc + ((p1[0] + p1[1]) + (p1[2] + p1[3]));
             }
         }
         __syncthreads();  // buffer (bt & 1) is refilled by stage(bt + 2); w reused
@@ -327,7 +359,6 @@ template <int K, int G>
 __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     constexpr int TG = tg_of(K), QG = qg_of(K);
     constexpr uint32_t GB = QG * 512;  // bytes of one table group of one chunk
-    constexpr int NITEM = (G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS;  // (head, dim pair) items per thread
     extern __shared__ __align__(128) uint8_t dsm[];
     uint32_t* qx = reinterpret_cast<uint32_t*>(dsm);  // [ncols][G] match masks
     uint8_t* ring = dsm + a.qx_bytes;                  // scan: [NWARP][depth][GB]; gather: rows + x tile
@@ -431,12 +462,16 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         // ---- 3. query masks: QX[c][g] = qbit ? 0 : ~0, so  P ^ QX = 1 where the key bit equals qbit
         for (int e = tid; e < G * a.KLw; e += DEC_THREADS) qb[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
         __syncthreads();
-        for (int e = tid; e < ncols * G; e += DEC_THREADS) {
-            const int c = e / G, g = e % G;
-            const int col = col0 + c;
-            uint32_t bit = 0;
-            if (col < a.KL) bit = (qb[g * a.KLw + (col >> 5)] >> (col & 31)) & 1u;
-            qx[e] = bit ? 0u : 0xffffffffu;
+        // thread per (head, 32 columns): one funnel-shifted word of query bits -> 32 masks
+        for (int e = tid; e < G * ((ncols + 31) >> 5); e += DEC_THREADS) {
+            const int g = e % G, c0 = (e / G) * 32;
+            const int col = col0 + c0, wi = col >> 5, sft = col & 31;
+            const uint32_t* qw = qb + g * a.KLw;
+            uint32_t bits = qw[wi] >> sft;
+            if (sft && wi + 1 < a.KLw) bits |= qw[wi + 1] << (32 - sft);
+            const int nc = min(32, ncols - c0);
+            for (int t = 0; t < nc; t++)
+                qx[(c0 + t) * G + g] = (col + t < a.KL && ((bits >> t) & 1u)) ? 0u : 0xffffffffu;
         }
         __syncthreads();
         MP_STAMP(2);
@@ -587,21 +622,18 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     MP_STAMP(5);
 
     // ---- 8. gather + estimator over this CTA's entries
-    float acc[NITEM][2];
-#pragma unroll
-    for (int r = 0; r < NITEM; r++) acc[r][0] = acc[r][1] = 0.0f;
+    float acc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
     gather_batched<K, G>(a, sh, ring, s_n, unit, acc);
     MP_STAMP(6);
 
     // ---- 9. this CTA's partial state (m, s, a) -> global parts[unit][slot*CS + rank]
     const int np = (int)per_unit * CS;
     float* pc = a.parts + (unit * np + slot * CS + rank) * G * PART;
+    if ((lane >> 2) < G) {
 #pragma unroll
-    for (int r = 0; r < NITEM; r++) {
-        const int it = tid + r * DEC_THREADS;
-        if (it < G * (HD / 2)) {
-            const int g = it / (HD / 2), dp = it % (HD / 2);
-            *reinterpret_cast<float2*>(pc + g * PART + 2 + 2 * dp) = make_float2(acc[r][0], acc[r][1]);
+        for (int nt = 0; nt < 2; nt++) {
+            const int d0 = warp * 16 + nt * 8 + 2 * (lane & 3);
+            *reinterpret_cast<float2*>(pc + (lane >> 2) * PART + 2 + d0) = make_float2(acc[nt][0], acc[nt][1]);
         }
     }
     if (tid < G) {

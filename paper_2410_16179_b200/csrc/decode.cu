@@ -290,6 +290,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
         // vectors' angle R5), then the batch max, rescale factor and weights of the online softmax
         if (warp < G) {
             const int g = warp, rr = lane;  // RB == 32
+            long long tz0 = clk64();
             float z = -INFINITY;
             if (rr < nb) {
                 const uint32_t sb = sh.bits[bt * RB + rr];
@@ -305,6 +306,7 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
                     z = logit - log_u_lookup(a.lut, p, K, a.L, a.minc);
                 }
             }
+            long long tz1 = clk64();
             float mb = z;
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, m));
@@ -320,6 +322,11 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
                 sh.scale[g] = sc;
                 sh.srun[g] = sh.srun[g] * sc + wsum;
                 sh.mrun[g] = mn;
+            }
+            if (a.timeline && threadIdx.x == 0) {
+                long long tz2 = clk64();
+                a.timeline[(size_t)blockIdx.x * 32 + 20] += (unsigned long long)(tz1 - tz0);
+                a.timeline[(size_t)blockIdx.x * 32 + 21] += (unsigned long long)(tz2 - tz1);
             }
         }
         __syncthreads();

@@ -273,8 +273,10 @@ def test_sequence_sharding_emulated():
             got = np.unpackbits(mk[0, row].view(np.uint8), bitorder="little")[: b - a]
             want = np.unpackbits(full["s_mask"][0, row].view(np.uint8), bitorder="little")[a:b]
             np.testing.assert_array_equal(got, want)
+    # same S and u; only the tf32 rounding of the softmax weights (relative 2^-11, taken
+    # against different running maxima per shard) differs between the two runs
     for row in range(4):
-        assert _rel_err(out.cpu().numpy()[0, row], full["out"][0, row]) <= 1e-5
+        assert _rel_err(out.cpu().numpy()[0, row], full["out"][0, row]) <= 2e-4
 
 
 def test_c2_full_size_sampled_unit():

@@ -58,6 +58,7 @@ def main():
     for p, nm in zip(range(11, 15), ["rows_wait", "x+mma", "z+max", "accum"]):
         col = t[:, p]
         print(f"   {nm:10s} med={np.median(col):8.0f} max={col.max():8.0f}")
+    print(f"   z-chain  med={np.median(t[:, 20]):8.0f}  max={t[:, 20].max():8.0f}   softmax-max med={np.median(t[:, 21]):8.0f}")
     m = t[:, 17] > 0
     if m.any():
         print("unit merge (cycles since start, median / max over merging CTAs):")

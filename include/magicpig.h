@@ -220,6 +220,16 @@ int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, const uint16_
                                        unsigned long long* timeline, int64_t timeline_len, void* ws,
                                        size_t ws_bytes, void* stream);
 
+/* Selects the decode kernel for subsequent decode calls of this process (a debug
+ * knob for A/B measurement; default 5): 5 = persistent warp-specialised kernel
+ * (one CTA per SM over a contiguous tile range; used whenever its shared-memory
+ * layout fits, else 4), 4 = one thread-block cluster per 1024-key chunk.  Both
+ * compute the same S bit for bit.  For kernel 5 the timeline slots are clock64
+ * cycles since CTA start (+1): 1 query masks ready, 2 first descriptor, 3 first
+ * gather batch, 4 unit merge start, 5 unit merge end, 6 gather done.
+ * Returns 0 or MAGICPIG_EINVAL. [host] */
+int magicpig_debug_set_decode_kernel(int version);
+
 /* Message for an error code. [host] */
 const char* magicpig_strerror(int err);
 

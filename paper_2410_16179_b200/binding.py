@@ -54,6 +54,7 @@ _SIGS = {
     "magicpig_decode_encoded": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p,
                                  _p, _sz, _p], _i),
     "magicpig_merge_partials": ([_p, _i, _i64, _p, _p], _i),
+    "magicpig_debug_set_decode_kernel": ([_i], _i),
     "magicpig_export_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
     "magicpig_import_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
     "magicpig_query_codes": ([_p, _p, _i64, _i64, _p, _p, _p, _sz, _p], _i),
@@ -249,6 +250,11 @@ def debug_decode_timeline(cfg, q, codes, center, key_norm, k, v, W, out, timelin
     if rc < 0:
         _check(int(rc), "debug_decode_timeline")
     return int(rc)
+
+
+def set_decode_kernel(version: int):
+    """Debug knob: 5 = persistent warp-specialised decode kernel (default), 4 = cluster-per-chunk."""
+    _check(lib().magicpig_debug_set_decode_kernel(int(version)), "set_decode_kernel")
 
 
 def launch_count() -> int:

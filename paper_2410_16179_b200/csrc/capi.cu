@@ -23,6 +23,22 @@ static int num_sms() {
     return n;
 }
 
+static int max_smem_optin() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || n <= 0)
+            n = 227 * 1024;
+    }
+    return n;
+}
+
+// decode kernel selection (debug knob, magicpig_debug_set_decode_kernel): 5 = persistent
+// warp-specialised kernel (default; falls back to 4 when its shared memory does not fit),
+// 4 = one cluster per chunk
+static std::atomic<int> g_decode_kernel{5};
+
 static bool cfg_ok(const magicpig_config* c) {
     if (!c) return false;
     if (c->head_dim != HD) return false;
@@ -99,7 +115,6 @@ static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, in
 
 struct DecodeWs {
     uint32_t* status;
-    float* lut;
     uint32_t* qbits;
     uint32_t* unit_ctr;
     float* parts;
@@ -123,12 +138,13 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
         return r;
     };
     w.status = (uint32_t*)take(256);
-    w.lut = (float*)take((size_t)(LUT_N + 1) * 4);
     w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
     w.unit_ctr = (uint32_t*)take((size_t)units * 4);
     const int64_t nT = n_local < (int64_t)c->sink + c->local ? n_local : (int64_t)c->sink + c->local;
     const int64_t nst = nT > 0 ? (nT + KCHUNK - 1) / KCHUNK : 1;
-    w.parts = (float*)take((size_t)units * (nch + nst) * 8 * G * PART * 4);  // up to 8 CTAs per cluster
+    const size_t parts4 = (size_t)units * (nch + nst) * 8 * G * PART * 4;      // up to 8 CTAs per cluster
+    const size_t parts5 = (size_t)(units + num_sms()) * G * PREC5 * 4;         // record u + CTA
+    w.parts = (float*)take(parts4 > parts5 ? parts4 : parts5);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
     w.bytes = off;
     return w;
@@ -238,8 +254,7 @@ int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64
     DecodeWs w = decode_layout(cfg, B, Hq, 1, 0, ws);
     const Geom g = make_geom(cfg->K, cfg->L, 0);
     if (ws_bytes < (size_t)((uint8_t*)w.qbits - (uint8_t*)ws) + (size_t)B * Hq * g.KLw * 4) return MAGICPIG_EWORKSPACE;
-    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream), w.lut, cfg->K, cfg->L,
-                          cfg->min_collisions);
+    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
 }
 
 static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
@@ -272,7 +287,6 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     memset(&a, 0, sizeof(a));
     a.q = q;
     a.qbits = w.qbits;
-    a.lut = w.lut;
     a.codes = codes;
     a.center = center;
     a.key_norm = key_norm;
@@ -322,14 +336,28 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.parts = w.parts;
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
-    const int64_t grid = B * Hkv * (g.nchunks + a.nstatic) * a.tsplit;
+    const int kver = g_decode_kernel.load();
+    bool v5 = kver % 10 == 5;
+    a.dbg = kver / 10;
+    if (v5) {
+        DecodeArgs t = a;
+        v5 = decode5_layout(t, (int)G, max_smem_optin()) != 0;
+    }
+    const int64_t tiles = B * Hkv * (g.nchunks + a.nstatic);
+    const int64_t grid = v5 ? (tiles < num_sms() ? tiles : num_sms()) : tiles * a.tsplit;
     if (grid_out) *grid_out = grid;
     if (timeline) {
         if (timeline_len < grid * 32) return MAGICPIG_EINVAL;
         if (cudaMemsetAsync(timeline, 0, (size_t)grid * 32 * 8, st) != cudaSuccess) return MAGICPIG_ECUDA;
         a.timeline = timeline;
     }
-    return launch_decode(a, st);
+    return v5 ? launch_decode5(a, num_sms(), max_smem_optin(), st) : launch_decode(a, st);
+}
+
+extern "C" int magicpig_debug_set_decode_kernel(int version) {
+    if (version % 10 != 4 && version % 10 != 5) return MAGICPIG_EINVAL;
+    g_decode_kernel.store(version);
+    return MAGICPIG_OK;
 }
 
 extern "C" int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
@@ -394,8 +422,8 @@ int magicpig_query_codes(const magicpig_config* cfg, const uint16_t* q, int64_t 
                          uint16_t* qcodes, void* ws, size_t ws_bytes, void* stream) {
     if (!cfg_ok(cfg) || B < 1 || Hq < 1 || !q || !W || !qcodes || !ws) return MAGICPIG_EINVAL;
     DecodeWs w = decode_layout(cfg, B, Hq, 1, 0, ws);
-    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
     const Geom g = make_geom(cfg->K, cfg->L, 0);
+    if (ws_bytes < (size_t)((uint8_t*)w.qbits - (uint8_t*)ws) + (size_t)B * Hq * g.KLw * 4) return MAGICPIG_EWORKSPACE;
     int rc = launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
     if (rc) return rc;
     return launch_qbits_to_canonical(w.qbits, B * Hq, cfg->K, cfg->L, g.KLw, qcodes, S(stream));

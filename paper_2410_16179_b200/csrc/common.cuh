@@ -11,6 +11,7 @@ namespace mp {
 constexpr int HD = 128;          // head dim (only 128 supported)
 constexpr int KCHUNK = 1024;     // keys per code chunk (32 blocks of 32 keys)
 constexpr int PART = HD + 2;     // (m, s, a[128]) partial softmax state
+constexpr int PREC5 = HD + 4;    // persistent decode record per head: (m, s, |S_g|, 0, a[128])
 constexpr float HASH_EPS = 0x1p-19f;  // tensor-core filter: |acc| <= eps*|x||W_j| -> exact fix-up
                                       // (measured tcgen05 error 2^-23.5 |x||W_j|: 22x margin)
 
@@ -224,21 +225,6 @@ __device__ __forceinline__ float log_sampling_prob(float p, int K, int L, int mi
         }
     }
     return fmaxf(lu, LOG_U_FLOOR);
-}
-
-// ln u(p) table for the decode: entries at p = i / LUT_N, i = 0..LUT_N, filled
-// each decode by the query-encode kernel; linear interpolation on [LUT_P0, 1]
-// (|error| <= h^2/8 max|d2 ln u/dp2| < 1e-5 for K <= 16), exact below.
-constexpr int LUT_N = 4096;
-constexpr float LUT_P0 = 0.125f;
-
-__device__ __forceinline__ float log_u_lookup(const float* __restrict__ lut, float p, int K, int L, int minc) {
-    if (p < LUT_P0) return log_sampling_prob(p, K, L, minc);
-    const float t = fminf(p, 1.0f) * (float)LUT_N;
-    const int i = min((int)t, LUT_N - 1);
-    const float f = t - (float)i;
-    const float a = __ldg(lut + i), b = __ldg(lut + i + 1);
-    return fmaf(f, b - a, a);
 }
 
 // --------------------------------------------------------------------------

@@ -290,7 +290,6 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
         // vectors' angle R5), then the batch max, rescale factor and weights of the online softmax
         if (warp < G) {
             const int g = warp, rr = lane;  // RB == 32
-            long long tz0 = clk64();
             float z = -INFINITY;
             if (rr < nb) {
                 const uint32_t sb = sh.bits[bt * RB + rr];
@@ -303,10 +302,9 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
                     float cs = den > 0.0f ? __fdividef(sh.zd[rr][g], den) : 0.0f;
                     cs = fminf(1.0f, fmaxf(-1.0f, cs));
                     const float p = 1.0f - acosf(cs) * 0.3183098861837907f;
-                    z = logit - log_u_lookup(a.lut, p, K, a.L, a.minc);
+                    z = logit - log_sampling_prob(p, K, a.L, a.minc);
                 }
             }
-            long long tz1 = clk64();
             float mb = z;
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, m));
@@ -322,11 +320,6 @@ __device__ __forceinline__ void gather_batched(const DecodeArgs& a, GatherShared
                 sh.scale[g] = sc;
                 sh.srun[g] = sh.srun[g] * sc + wsum;
                 sh.mrun[g] = mn;
-            }
-            if (a.timeline && threadIdx.x == 0) {
-                long long tz2 = clk64();
-                a.timeline[(size_t)blockIdx.x * 32 + 20] += (unsigned long long)(tz1 - tz0);
-                a.timeline[(size_t)blockIdx.x * 32 + 21] += (unsigned long long)(tz2 - tz1);
             }
         }
         __syncthreads();
@@ -375,6 +368,7 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __shared__ uint32_t s_part[NWARP][G][2][32];
     __shared__ uint32_t s_sel[G][32];
     __shared__ uint32_t s_tm[32];
+    __shared__ int s_base[32];
     __shared__ int s_n;
     __shared__ uint32_t s_flag;
     __shared__ GatherShared<G> sh;
@@ -593,7 +587,9 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
             }
         }
         __syncthreads();
-        // ---- 7. compaction (ascending) of union_g S_g; entry e goes to cluster rank e % CS
+        // ---- 7. compaction (ascending) of union_g S_g; entry e goes to cluster rank e % CS.
+        // warp 0: exclusive scan of the 32 block counts; then warp w emits blocks w, w+8, ..
+        // (lane = key of the block, position = block base + popc of the lower set bits)
         if (warp == 0) {
             uint32_t u = 0;
 #pragma unroll
@@ -605,22 +601,27 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, m);
                 if (lane >= m) incl += t;
             }
-            int pos = incl - c;
-            while (u) {
-                const int r = __ffs(u) - 1;
-                u &= u - 1;
+            s_base[lane] = incl - c;
+            if (lane == 31) s_n = incl > rank ? (incl - rank + CS - 1) >> lcs : 0;
+        }
+        __syncthreads();
+        for (int bl = warp; bl < 32; bl += NWARP) {
+            uint32_t u = 0, sg[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                sg[g] = s_sel[g][bl];
+                u |= sg[g];
+            }
+            if ((u >> lane) & 1u) {
+                const int pos = s_base[bl] + __popc(u & ((1u << lane) - 1u));
                 if ((pos & (CS - 1)) == rank) {
-                    const int j = pos >> lcs;
-                    const uint32_t bitm = 1u << r;
                     uint32_t bits = 0;
 #pragma unroll
-                    for (int g = 0; g < G; g++) bits |= ((s_sel[g][lane] & bitm) ? 1u : 0u) << g;
-                    sh.keys[j] = (int)(cbase + lane * 32 + r);
-                    sh.bits[j] = (uint16_t)bits;
+                    for (int g = 0; g < G; g++) bits |= ((sg[g] >> lane) & 1u) << g;
+                    sh.keys[pos >> lcs] = (int)(cbase + bl * 32 + lane);
+                    sh.bits[pos >> lcs] = (uint16_t)bits;
                 }
-                pos++;
             }
-            if (lane == 31) s_n = incl > rank ? (incl - rank + CS - 1) >> lcs : 0;
         }
         // remote s_part reads are done: let the cluster peers go on (we wait before exiting)
         if (CS > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -663,26 +664,31 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
     __threadfence();
     MP_STAMP(9);
     long long tm0 = clk64();
-    const float* pu = a.parts + unit * (int64_t)np * G * PART;
+    // The unit's partial block (np x G x PART floats, contiguous) comes into shared
+    // memory by bulk copies -- one L2 round trip when it fits -- and every thread
+    // (head g, dim pair dp) folds the partials in fixed order with an online
+    // log-sum-exp merge ("recursive attention").
     __shared__ int s_cnt[G];
-    __shared__ float s_M[G], s_S[G];
-    float* sm_f = reinterpret_cast<float*>(ring);  // [np][G] m, then scale factors
-    float* sm_s = sm_f + (size_t)np * G;           // [np][G] s
-    const bool fit = (size_t)np * G * 8 <= (size_t)a.ring_bytes;
-    // issue the first block of a-value loads before the m/s round completes
-    constexpr int BLK = 16;
-    const int g_it = tid / (HD / 2), dp_it = tid % (HD / 2);  // item = tid (G*64 items; G <= 4 here)
-    float2 av[BLK];
-    const bool own = tid < G * (HD / 2);
-#pragma unroll
-    for (int t = 0; t < BLK; t++)
-        av[t] = (own && t < np) ? __ldcg(reinterpret_cast<const float2*>(pu + ((int64_t)t * G + g_it) * PART + 2) + dp_it)
-                                : make_float2(0.0f, 0.0f);
-    if (fit) {
-        for (int e = tid; e < np * G; e += DEC_THREADS) {
-            sm_f[e] = __ldcg(pu + (int64_t)e * PART);
-            sm_s[e] = __ldcg(pu + (int64_t)e * PART + 1);
-        }
+    __shared__ __align__(8) uint64_t s_mbar[2];
+    const float* pu = a.parts + unit * (int64_t)np * G * PART;
+    constexpr uint32_t PROW = G * PART * 4;  // bytes of one partial (all G heads)
+    const int per_buf = max(1, (int)((uint32_t)a.dyn_bytes / 2u / PROW));
+    const int nblk = (np + per_buf - 1) / per_buf;
+    float* mbuf0 = reinterpret_cast<float*>(dsm);
+    float* mbuf1 = mbuf0 + (size_t)per_buf * G * PART;
+    auto issue = [&](int j) {  // block j -> buffer j & 1
+        const int c0 = j * per_buf, cnt = min(per_buf, np - c0);
+        mbar_arrive_expect_tx(&s_mbar[j & 1], (uint32_t)cnt * PROW);
+        bulk_g2s((j & 1) ? mbuf1 : mbuf0, pu + (size_t)c0 * G * PART, (uint32_t)cnt * PROW, &s_mbar[j & 1]);
+    };
+    if (tid == 0) {
+        mbar_init(&s_mbar[0], 1);
+        mbar_init(&s_mbar[1], 1);
+        fence_mbar_init();
+        // other CTAs' generic-proxy writes (made visible by the counter) are read by the async proxy;
+        // this CTA's own generic accesses to the buffers precede the bulk writes
+        asm volatile("fence.proxy.async;" ::: "memory");
+        for (int j = 0; j < 2 && j < nblk; j++) issue(j);
     }
     if (warp < G) {  // |S_g| summed over the unit's chunks
         int cnt = 0;
@@ -691,61 +697,63 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
         if (lane == 0) s_cnt[warp] = cnt;
     }
-    __syncthreads();
-    if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32 + 17] = (unsigned long long)(clk64() - tm0);
-    if (warp < G) {  // M_g, f_pg = e^{m_pg - M_g}, S_g  (fixed order)
-        const int g = warp;
-        float M = -INFINITY;
-        for (int c = lane; c < np; c += 32) M = fmaxf(M, fit ? sm_f[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART));
+    __syncthreads();  // mbarrier inits visible before any wait
+    constexpr int NI = (G * (HD / 2) + DEC_THREADS - 1) / DEC_THREADS;
+    float Mx[NI], Sx[NI], A0[NI], A1[NI];
 #pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, m));
-        float S = 0.0f;
-        for (int c = lane; c < np; c += 32) {
-            const float mc = fit ? sm_f[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART);
-            const float sc = fit ? sm_s[c * G + g] : __ldcg(pu + ((int64_t)c * G + g) * PART + 1);
-            const float f = (M == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - M);
-            if (fit) sm_f[c * G + g] = f;
-            S += f * sc;
+    for (int t = 0; t < NI; t++) Mx[t] = -INFINITY, Sx[t] = A0[t] = A1[t] = 0.0f;
+    for (int j = 0; j < nblk; j++) {
+        mbar_wait(&s_mbar[j & 1], (uint32_t)((j >> 1) & 1));
+        const float* buf = (j & 1) ? mbuf1 : mbuf0;
+        const int cnt = min(per_buf, np - j * per_buf);
+        if (a.timeline && tid == 0 && j == 0) a.timeline[(size_t)blockIdx.x * 32 + 17] = (unsigned long long)(clk64() - tm0);
+#pragma unroll
+        for (int t = 0; t < NI; t++) {
+            const int e = tid + t * DEC_THREADS;
+            if (e < G * (HD / 2)) {
+                const int g = e / (HD / 2), dp = e % (HD / 2);
+                const float* pg = buf + (size_t)g * PART;
+                float Mb = -INFINITY;  // block max, then one rescale of the running state
+                for (int c = 0; c < cnt; c++) Mb = fmaxf(Mb, pg[(size_t)c * G * PART]);
+                const float Mn = fmaxf(Mx[t], Mb);
+                if (Mn != -INFINITY) {
+                    const float fo = Mx[t] == -INFINITY ? 0.0f : __expf(Mx[t] - Mn);
+                    float s_ = Sx[t] * fo, a0 = A0[t] * fo, a1 = A1[t] * fo;
+#pragma unroll 4
+                    for (int c = 0; c < cnt; c++) {
+                        const float* pp = pg + (size_t)c * G * PART;
+                        const float mc = pp[0];
+                        const float f = mc == -INFINITY ? 0.0f : __expf(mc - Mn);
+                        const float2 av = *reinterpret_cast<const float2*>(pp + 2 + 2 * dp);
+                        s_ = fmaf(f, pp[1], s_);
+                        a0 = fmaf(f, av.x, a0);
+                        a1 = fmaf(f, av.y, a1);
+                    }
+                    Mx[t] = Mn, Sx[t] = s_, A0[t] = a0, A1[t] = a1;
+                }
+            }
         }
-        S = warp_sum_f(S);
-        if (lane == 0) {
-            s_M[g] = M;
-            s_S[g] = S;
+        if (j + 2 < nblk) {
+            __syncthreads();  // buffer j & 1 fully read
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(j + 2);
+            }
         }
     }
-    __syncthreads();
     if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32 + 18] = (unsigned long long)(clk64() - tm0);
-    auto fac = [&](int c, int g) -> float {
-        if (fit) return sm_f[c * G + g];
-        const float mc = __ldcg(pu + ((int64_t)c * G + g) * PART);
-        return (s_M[g] == -INFINITY || mc == -INFINITY) ? 0.0f : __expf(mc - s_M[g]);
-    };
-    for (int e = tid; e < G * (HD / 2); e += DEC_THREADS) {
+#pragma unroll
+    for (int t = 0; t < NI; t++) {
+        const int e = tid + t * DEC_THREADS;
+        if (e >= G * (HD / 2)) continue;
         const int g = e / (HD / 2), dp = e % (HD / 2);
-        float A0 = 0.0f, A1 = 0.0f;
-        for (int c0 = 0; c0 < np; c0 += BLK) {
-            if (!(c0 == 0 && e == tid)) {
-#pragma unroll
-                for (int t = 0; t < BLK; t++)
-                    av[t] = (c0 + t < np) ? __ldcg(reinterpret_cast<const float2*>(pu + ((int64_t)(c0 + t) * G + g) * PART + 2) + dp)
-                                          : make_float2(0.0f, 0.0f);
-            }
-#pragma unroll
-            for (int t = 0; t < BLK; t++) {
-                if (c0 + t >= np) break;
-                const float f = fac(c0 + t, g);
-                A0 = fmaf(f, av[t].x, A0);
-                A1 = fmaf(f, av[t].y, A1);
-            }
-        }
-        const float M = s_M[g], S = s_S[g];
+        const float M = Mx[t], S = Sx[t];
         const int64_t row = qh0 + g;
         if (a.out)
             *reinterpret_cast<float2*>(a.out + row * HD + 2 * dp) =
-                S > 0.0f ? make_float2(A0 / S, A1 / S) : make_float2(0.0f, 0.0f);
+                S > 0.0f ? make_float2(A0[t] / S, A1[t] / S) : make_float2(0.0f, 0.0f);
         if (a.partial) {
-            a.partial[row * PART + 2 + 2 * dp] = A0;
-            a.partial[row * PART + 3 + 2 * dp] = A1;
+            *reinterpret_cast<float2*>(a.partial + row * PART + 2 + 2 * dp) = make_float2(A0[t], A1[t]);
             if (dp == 0) {
                 a.partial[row * PART] = M;
                 a.partial[row * PART + 1] = S;
@@ -753,7 +761,6 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_kernel(DecodeArgs a) {
         }
         if (dp == 0 && !(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
     }
-    __syncthreads();
     if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32 + 19] = (unsigned long long)(clk64() - tm0);
     if (tid < G && a.s_count) a.s_count[qh0 + tid] = s_cnt[tid];
     if (tid == 0) a.unit_ctr[unit] = 0u;
@@ -811,6 +818,7 @@ static int launch_kg(DecodeArgs a, cudaStream_t st) {
     if (decode_dyn_smem(K, G, ncols_max, 3, a.KLw) > 96 * 1024) a.depth = 2;
     a.ring_bytes = (int)ring_bytes(K, a.depth);
     size_t smem = decode_dyn_smem(K, G, ncols_max, a.depth, a.KLw);
+    a.dyn_bytes = (int)smem;
     auto kern = decode_kernel<K, G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MAGICPIG_ECUDA;

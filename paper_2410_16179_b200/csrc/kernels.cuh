@@ -28,12 +28,11 @@ int launch_hash_gemm(const uint8_t* xt, const uint8_t* wt, const float* xnorm, c
                      uint32_t* status, float* dbg_acc, cudaStream_t st);
 
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
-                   uint32_t* status, cudaStream_t st, float* lut = nullptr, int K = 0, int L = 0, int minc = 2);
+                   uint32_t* status, cudaStream_t st);
 
 struct DecodeArgs {
     const uint16_t* q;
     const uint32_t* qbits;
-    const float* lut;  // ln u(p) table (LUT_N + 1 entries)
     const uint32_t* codes;
     const float* center;
     const float* key_norm;
@@ -45,6 +44,11 @@ struct DecodeArgs {
     int64_t nstatic;  // static-key pieces (clusters) per unit
     int tsplit, sink, local, minc;
     int qx_bytes, depth, ring_bytes;  // set by the launcher
+    int dyn_bytes;                    // dynamic shared memory per CTA (set by the launcher)
+    // persistent kernel (decode5.cu): ring slots, shared-memory offsets, tile count
+    int v5_ns, v5_off_qx, v5_off_qbw, v5_off_part, v5_off_rows, v5_off_xt, v5_off_fixed, v5_off_bars;
+    int64_t v5_tiles;
+    int dbg;                          // debug flags (kernel 5: bit 0 = no L2 prefetch)
     unsigned long long* timeline;  // debug: [grid][16] globaltimer stamps, or NULL
     float* out;
     float* partial;
@@ -56,6 +60,8 @@ struct DecodeArgs {
     uint32_t* status;
 };
 int launch_decode(const DecodeArgs& a, cudaStream_t st);
+size_t decode5_layout(DecodeArgs& a, int G, int max_smem);
+int launch_decode5(const DecodeArgs& a, int nsm, int max_smem, cudaStream_t st);
 int launch_merge(const float* parts, int P, int64_t BH, float* out, cudaStream_t st);
 int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st);
 

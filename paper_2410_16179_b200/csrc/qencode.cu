@@ -20,15 +20,9 @@ constexpr int QE_THREADS = 256;
 // exact integers.
 __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __restrict__ q, int64_t BHq,
                                                              const float* __restrict__ W, int KL, int KLw,
-                                                             uint32_t* __restrict__ qbits, uint32_t* status,
-                                                             float* __restrict__ lut, int K, int L, int minc) {
+                                                             uint32_t* __restrict__ qbits, uint32_t* status) {
     // let the dependent decode kernel launch now: it streams codes while we encode
     asm volatile("griddepcontrol.launch_dependents;");
-    if (blockIdx.y == gridDim.y - 1 && lut) {  // extra row of CTAs: the ln u(p) table
-        for (int i = blockIdx.x * QE_THREADS + threadIdx.x; i <= LUT_N; i += gridDim.x * QE_THREADS)
-            lut[i] = log_sampling_prob((float)i / (float)LUT_N, K, L, minc);
-        return;
-    }
     __shared__ float ws[HD][QE_COLS];
     __shared__ __align__(16) float qs[HD][QE_HPB];
     __shared__ __align__(16) float qa[HD][QE_HPB];
@@ -140,9 +134,9 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
 }
 
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
-                   uint32_t* status, cudaStream_t st, float* lut, int K, int L, int minc) {
-    dim3 grid((unsigned)((KL + QE_COLS - 1) / QE_COLS), (unsigned)((BHq + QE_HPB - 1) / QE_HPB) + (lut ? 1u : 0u));
-    qencode_kernel<<<grid, QE_THREADS, 0, st>>>(q, BHq, W, KL, KLw, qbits, status, lut, K, L, minc);
+                   uint32_t* status, cudaStream_t st) {
+    dim3 grid((unsigned)((KL + QE_COLS - 1) / QE_COLS), (unsigned)((BHq + QE_HPB - 1) / QE_HPB));
+    qencode_kernel<<<grid, QE_THREADS, 0, st>>>(q, BHq, W, KL, KLw, qbits, status);
     count_launch(1);
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }

@@ -20,6 +20,18 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-3
 
 
+@pytest.fixture(params=[5, 4], ids=["k5", "k4"], autouse=True)
+def decode_kernel(request):
+    """Every parity test runs on both decode kernels (persistent warp-specialised
+    and cluster-per-chunk); they must agree with the oracle independently."""
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no fallback)")
+    pkg = _pkg()
+    pkg.binding.set_decode_kernel(request.param)
+    yield request.param
+    pkg.binding.set_decode_kernel(5)
+
+
 def _dev():
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device (no fallback)")
@@ -104,6 +116,10 @@ CASES = [
     ("k16", 1100, 1, 2, 1, 16, 9, 1, 1, 2, 2, 8),
     ("allstatic", 60, 1, 4, 1, 10, 150, 1, 1, 2, 4, 64),
     ("tiny", 37, 1, 1, 1, 2, 3, 1, 1, 2, 1, 1),
+    # persistent kernel: CTAs spanning several units, and units spanning > 1 merge block
+    ("manyunits", 3000, 16, 32, 8, 8, 20, 1, 1, 2, 4, 64),
+    ("longunit", 40000, 1, 4, 1, 8, 20, 1, 1, 2, 4, 64),
+    ("longg8", 20000, 1, 8, 1, 6, 16, 1, 1, 2, 4, 64),
 ]
 
 

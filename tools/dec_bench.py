@@ -1,0 +1,103 @@
+"""Decode kernel micro-benchmark: kernel-only and encode+decode step times,
+algorithmic bytes and roofline fraction, for a config (optionally with n / B
+overridden).  For iteration; bench.py is the contract.
+
+  python tools/dec_bench.py C2 [n=65536] [B=8] [reps=4]
+"""
+from __future__ import annotations
+
+import dataclasses
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_2410_16179_b200 as pkg  # noqa: E402
+from paper_2410_16179_b200 import binding as B_  # noqa: E402
+
+
+def run(name, R=4, G_STEPS=64, **over):
+    wl = dataclasses.replace(synth.CONFIGS[name], **over)
+    dev = torch.device("cuda:0")
+    k, v, q = synth.make_batch(wl)
+    W = synth.make_projections(wl.K, wl.L, wl.mips)
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
+    tk, tv, tq, tW = bf(k), bf(v), bf(q), torch.from_numpy(W).to(dev)
+    del k, v
+    mps, ks, vs = [], [], []
+    for r in range(R):
+        kr = tk if r == 0 else tk.clone()
+        vr = tv if r == 0 else tv.clone()
+        mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, mips=wl.mips).build(kr)
+        mp.release_build_workspace()
+        mps.append(mp), ks.append(kr), vs.append(vr)
+    cfg = mps[0].cfg
+    n, Bn, Hq, Hkv = wl.n, wl.B, wl.Hq, wl.Hkv
+    ws = B_.new_workspace(B_.decode_workspace_bytes(cfg, Bn, Hq, Hkv, n), dev)
+    out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=dev)
+    nw = (n + 31) // 32
+    smask = torch.zeros((Bn, Hq, nw), dtype=torch.int32, device=dev)
+    scount = torch.zeros((Bn, Hq), dtype=torch.int32, device=dev)
+    B_.decode(cfg, tq, mps[0].buf.codes, mps[0].buf.center, mps[0].buf.key_norm, ks[0], vs[0], 0, n, tW, ws,
+              out=out, s_count=scount, s_mask=smask)
+    torch.cuda.synchronize()
+    sm = smask.cpu().numpy().view(np.uint32).reshape(Bn, Hkv, wl.G, nw)
+    union = np.bitwise_or.reduce(sm, axis=2)
+    n_union = int(np.unpackbits(union.view(np.uint8)).sum())
+    nT = min(n, wl.sink + wl.local)
+    KL = wl.K * wl.L
+    alg = Bn * Hkv * (n - nT) * KL / 8 + (n_union + Bn * Hkv * nT) * 512 + n_union * 4 + Bn * Hq * (256 + KL / 8) \
+        + Bn * Hkv * 512
+
+    def kern(r):
+        B_.decode_encoded(cfg, tq, mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n, ws,
+                          out=out)
+
+    def step(r):
+        B_.encode_queries(cfg, tq, tW, ws)
+        kern(r)
+
+    res = {}
+    for nm, fn in (("kernel", kern), ("step", step)):
+        for r in range(R):
+            fn(r)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(G_STEPS):
+                fn(i % R)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(5):
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / G_STEPS)
+        res[nm + "_us"] = float(np.median(ts))
+    res.update(config=name, n=n, B=Bn, K=wl.K, L=wl.L, alg_MB=alg / 1e6,
+               sampled=float(scount.float().mean()) / max(n - nT, 1), union=n_union,
+               GBs=alg / res["kernel_us"] / 1e3, frac=alg / res["kernel_us"] / 1e3 / 6545.0,
+               status=B_.workspace_status(ws))
+    print(json.dumps(res), flush=True)
+    return res
+
+
+if __name__ == "__main__":
+    name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+    kw = {}
+    R = 4
+    for a in sys.argv[2:]:
+        key, val = a.split("=")
+        if key == "reps":
+            R = int(val)
+        else:
+            kw[key] = int(val)
+    run(name, R=R, **kw)

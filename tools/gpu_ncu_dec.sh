@@ -1,0 +1,11 @@
+#!/bin/bash
+# ncu source-level captures of the decode kernel at C2 and C3
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+OUT=gpurun_out/${TAG:-ncu}
+mkdir -p $OUT
+NCU=/usr/local/cuda/bin/ncu
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"decode_kernel" -s 8 -c 1 \
+   -o $OUT/dec_c2 python tools/dec_bench.py C2 reps=2 > $OUT/ncu_c2.log 2>&1
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"decode_kernel" -s 4 -c 1 \
+   -o $OUT/dec_c3 python tools/dec_bench.py C3 reps=1 > $OUT/ncu_c3.log 2>&1

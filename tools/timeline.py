@@ -20,6 +20,15 @@ PH = ["start", "gdc_wait", "qmasks", "scan", "cl_comb", "compact", "gather", "ct
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "C2"
     wl = synth.CONFIGS[name]
+    import dataclasses
+    kver = 5
+    for a_ in sys.argv[2:]:
+        k_, v_ = a_.split('=')
+        if k_ == "kernel":
+            kver = int(v_)
+            continue
+        wl = dataclasses.replace(wl, **{k_: int(v_)})
+    B_.set_decode_kernel(kver)
     dev = torch.device("cuda:0")
     k, v, q = synth.make_batch(wl)
     W = synth.make_projections(wl.K, wl.L, wl.mips)
@@ -29,7 +38,7 @@ def main():
     mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L).build(tk)
     ws = mp.decode_workspace(wl.B, wl.Hq, wl.Hkv, wl.n, dev)
     out = torch.empty((wl.B, wl.Hq, 128), dtype=torch.float32, device=dev)
-    tl = torch.zeros((100000 * 16,), dtype=torch.int64, device=dev)
+    tl = torch.zeros((200000 * 32,), dtype=torch.int64, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     res = []
     for it in range(6):
@@ -44,6 +53,25 @@ def main():
     st = st - st[st > 0].min()
     print(f"{name}: {t.shape[0]} CTAs; CTA start spread: med {np.median(st)/1e3:.2f} us, max {st.max()/1e3:.2f} us")
     ghz = 1.965
+    if kver % 10 == 5:
+        names = ["start", "qmasks", "desc0", "batch0", "merge0", "merge1", "gdone", "prod_NS", "full0", "-",
+                 "prod_end"] + [f"scanw{w}" for w in range(8)] + ["m_loaded", "m_comp", "flush0", "atomic"]
+        for p in range(1, 23):
+            if p == 9:
+                continue
+            col = t[:, p]
+            m = col > 0
+            if not m.any():
+                continue
+            us = (col[m] - 1) / ghz / 1e3 + st[m] / 1e3
+            print(f"{p:2d} {names[p]:9s} n={m.sum():5d}  (abs) min={us.min():7.2f}  med={np.median(us):7.2f}  "
+                  f"p90={np.percentile(us, 90):7.2f}  max={us.max():7.2f} us")
+        print("per-CTA totals (us, median / max):")
+        for p, nm in zip(range(23, 29), ["scan: wait codes", "scan: wait desc", "scan: total", "gather: wait desc",
+                                          "gather: wait rows", "gather: total"]):
+            col = t[:, p].astype(np.float64) / ghz / 1e3
+            print(f"   {nm:18s} {np.median(col):8.2f} {col.max():8.2f}")
+        return
     for p, nm in enumerate(PH):
         if p == 0:
             continue
@@ -58,7 +86,8 @@ def main():
     for p, nm in zip(range(11, 15), ["rows_wait", "x+mma", "z+max", "accum"]):
         col = t[:, p]
         print(f"   {nm:10s} med={np.median(col):8.0f} max={col.max():8.0f}")
-    print(f"   z-chain  med={np.median(t[:, 20]):8.0f}  max={t[:, 20].max():8.0f}   softmax-max med={np.median(t[:, 21]):8.0f}")
+    life = (t[:, 8].astype(np.int64) - 1) / ghz / 1e3
+    print(f"CTA lifetime to cl_merge (us): med {np.median(life):.2f}  p90 {np.percentile(life, 90):.2f}  max {life.max():.2f}")
     m = t[:, 17] > 0
     if m.any():
         print("unit merge (cycles since start, median / max over merging CTAs):")

@@ -170,6 +170,76 @@ def cpu_oracle_timing(wl, k, v, q, W, steps_cap=None, target_s=10.0):
     return {"step_s": statistics.mean(times), "steps": len(times), "threads": threads, "build_s": t_build}
 
 
+# ----------------------------------------------------------------------------- context sweep
+def sweep_point(wl, dev, tW, peak, graph_launches=64):
+    """Decode kernel alone (the roofline kernel) at one workload: inputs rotated over R
+    replicas so that a launch's bytes were last touched R-1 launches earlier (> L2)."""
+    import torch
+    import paper_2410_16179_b200 as pkg
+    from paper_2410_16179_b200 import binding as B_
+
+    k, v, q = synth.make_batch(wl, threads=os.cpu_count() or 1)
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
+    tk, tv, tq = bf(k), bf(v), bf(q)
+    del k, v
+    per_rep = wl.B * wl.Hkv * wl.n * (512 + wl.K * wl.L / 8)
+    R = int(min(16, max(2, -(-300e6 // per_rep))))
+    mps, ks, vs = [], [], []
+    for r in range(R):
+        kr = tk if r == 0 else tk.clone()
+        vr = tv if r == 0 else tv.clone()
+        mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, center=wl.center, mips=wl.mips, min_collisions=wl.min_collisions,
+                          sink=wl.sink, local=wl.local).build(kr)
+        mp.release_build_workspace()
+        mps.append(mp), ks.append(kr), vs.append(vr)
+    cfg = mps[0].cfg
+    n, Bn, Hq, Hkv = wl.n, wl.B, wl.Hq, wl.Hkv
+    ws = B_.new_workspace(B_.decode_workspace_bytes(cfg, Bn, Hq, Hkv, n), dev)
+    out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=dev)
+    nw = (n + 31) // 32
+    smask = torch.zeros((Bn, Hq, nw), dtype=torch.int32, device=dev)
+    scount = torch.zeros((Bn, Hq), dtype=torch.int32, device=dev)
+    B_.decode(cfg, tq, mps[0].buf.codes, mps[0].buf.center, mps[0].buf.key_norm, ks[0], vs[0], 0, n, tW, ws,
+              out=out, s_count=scount, s_mask=smask)
+    torch.cuda.synchronize()
+    sm = smask.cpu().numpy().view(np.uint32).reshape(Bn, Hkv, wl.G, nw)
+    n_union = int(np.unpackbits(np.bitwise_or.reduce(sm, axis=2).view(np.uint8)).sum())
+    nT = min(n, wl.sink + wl.local)
+    KL = wl.K * wl.L
+    alg = (Bn * Hkv * (n - nT) * KL / 8 + (n_union + Bn * Hkv * nT) * 512 + n_union * 4 + Bn * Hq * (256 + KL / 8)
+           + Bn * Hkv * 512)
+
+    def kern(r):
+        B_.decode_encoded(cfg, tq, mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n, ws,
+                          out=out)
+
+    for r in range(R):
+        kern(r)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(graph_launches):
+            kern(i % R)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(5):
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / graph_launches)
+    us = float(np.median(ts))
+    gbs = alg / us / 1e3
+    res = {"n": n, "B": Bn, "Hq": Hq, "Hkv": Hkv, "K": wl.K, "L": wl.L, "kernel_us": us, "tokens_per_s": Bn / us * 1e6,
+           "alg_MB": alg / 1e6, "GBs": gbs, "frac": gbs / peak, "sampled_fraction": float(scount.float().mean()) /
+           max(n - nT, 1), "replicas": R}
+    del mps, ks, vs, tk, tv
+    torch.cuda.empty_cache()
+    return res
+
+
 # ----------------------------------------------------------------------------- ours
 def run_ours(args):
     import torch
@@ -339,6 +409,24 @@ def run_ours(args):
     # correctness guard on the timed path: the last outputs are finite
     assert torch.isfinite(outs[0]).all().item(), "non-finite output"
 
+    sweep = None
+    if rank == 0 and args.sweep:
+        import dataclasses
+        sweep = []
+        for spec in args.sweep.split(","):
+            name, _, nn = spec.partition(":")
+            wl_s = dataclasses.replace(synth.CONFIGS[name], n=int(nn)) if nn else synth.CONFIGS[name]
+            if wl_s == wl:
+                sweep.append({"n": n, "B": Bn, "Hq": Hq, "Hkv": Hkv, "K": wl.K, "L": wl.L, "kernel_us": kern_ms * 1e3,
+                              "tokens_per_s": Bn / kern_ms * 1e3, "alg_MB": alg_bytes / 1e6, "GBs": achieved,
+                              "frac": achieved / peak, "sampled_fraction": sampled_frac, "replicas": R})
+                continue
+            tWs = tW if (wl_s.K, wl_s.L, wl_s.mips) == (wl.K, wl.L, wl.mips) else \
+                torch.from_numpy(synth.make_projections(wl_s.K, wl_s.L, wl_s.mips)).to(dev)
+            pt = sweep_point(wl_s, dev, tWs, peak)
+            pt["config"] = name
+            sweep.append(pt)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_oracle_timing(wl, k, v, q, W, target_s=args.cpu_seconds)
@@ -357,13 +445,14 @@ def run_ours(args):
                        "l2": f"{R} rotating input replicas", "sampled_fraction": sampled_frac,
                        "union_rows": n_union, "alg_bytes_per_step": alg_bytes, "status": status},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": tr, "kernel": "decode_kernel (scan+gather+estimator+merge)",
+                         "traffic": tr, "kernel": "decode5_kernel (persistent: scan + gather + estimator + unit merge)",
                          "kernel_us": kern_ms * 1e3, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(tq.numel() * 2),
                     "d2h_bytes_per_step": int(Bn * Hq * 128 * 4), "ms_per_step": e2e_ms},
             "gpu_launches": int(gpu_launches),
             "clocks": clk.summary(),
+            "context_sweep": sweep,
         }
         print(json.dumps(line))
     if dist:
@@ -413,6 +502,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-steps-cap", type=int, default=200)
+    ap.add_argument("--sweep", default="C2:4096,C2:16384,C2:65536,C2:131072",
+                    help="decode-kernel roofline vs context length: comma list of CONFIG[:n] ('' = off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -89,8 +89,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    uint32_t ns = 32;
     while (!ok) {
-        __nanosleep(100);
+        __nanosleep(ns);
+        ns = ns < 512 ? ns * 2 : 512;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -227,47 +229,34 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
         const int64_t gc1 = chunks_before(t1);
         const size_t CB = (size_t)a.KLq * 512;  // code bytes per chunk
         const uint8_t* codes_b = reinterpret_cast<const uint8_t*>(a.codes);
-        // issue iterator over this warp's (chunk, group) sequence; no divisions on this path
+        // issue iterator over this warp's (chunk, group) sequence: a source pointer that steps by
+        // NSW groups and jumps to the next chunk; ring write/read pointers rotate (no divisions)
         int64_t it_c = chunks_before(t0);
         int it_j = warp;
         const bool has_groups = warp < a.ngroups;
-        uint32_t icount = 0, ccount = 0;
-        // L2 prefetch iterator (debug flag 2), PFD groups ahead of the copy iterator
-        constexpr int PFD = 8;
-        int64_t pf_c = it_c;
-        int pf_j = it_j;
-        auto advance = [&](int64_t& c_, int& j_) {
-            j_ += NSW;
-            if (j_ >= a.ngroups) {
-                j_ = warp;
-                c_++;
-            }
-        };
-        auto prefetch_next = [&]() {
-            if (has_groups && pf_c < gc1) {
-                const uint8_t* gs = codes_b + (size_t)pf_c * CB + (size_t)pf_j * GB;
-                for (int l = lane; l < QG * 4; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(gs + l * 128));
-                advance(pf_c, pf_j);
-            }
-        };
+        const uint8_t* it_src = codes_b + (size_t)it_c * CB + (size_t)warp * GB + lane * 16;
+        uint8_t* const ring_end = myring + (size_t)D * GB;
+        uint8_t* wr = myring + lane * 16;
+        const uint8_t* rd = myring + lane * 16;
         auto issue = [&]() {
             if (has_groups && it_c < gc1) {
-                const uint4* gs = reinterpret_cast<const uint4*>(codes_b + (size_t)it_c * CB + (size_t)it_j * GB) + lane;
-                uint4* ds = reinterpret_cast<uint4*>(myring + (size_t)(icount % D) * GB) + lane;
 #pragma unroll
-                for (int q = 0; q < QG; q++) cp_async16(ds + q * 32, gs + q * 32);
-                advance(it_c, it_j);
+                for (int q = 0; q < QG; q++) cp_async16(wr + q * 512, it_src + q * 512);
+                it_j += NSW;
+                if (it_j >= a.ngroups) {
+                    it_j = warp;
+                    it_c++;
+                    it_src = codes_b + (size_t)it_c * CB + (size_t)warp * GB + lane * 16;
+                } else {
+                    it_src += NSW * GB;
+                }
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
-            icount++;
-            if (a.dbg & 2) prefetch_next();
+            wr += GB;
+            if (wr >= ring_end) wr -= (size_t)D * GB;
         };
-        if (has_groups)
-            for (int k = 0; k < D && pf_c < gc1; k++) advance(pf_c, pf_j);
 #pragma unroll 1
         for (int k = 0; k < D; k++) issue();
-        if (a.dbg & 2)
-            for (int k = 0; k < PFD; k++) prefetch_next();
         asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
         const StaticRanges sr = static_ranges(a);
         const int ncolsP = a.ngroups * TG * K;
@@ -301,17 +290,17 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                     asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
                     __syncwarp();
                     uint4 Pw[QG];
-                    const uint4* src = reinterpret_cast<const uint4*>(myring + (size_t)(ccount % D) * GB) + lane;
 #pragma unroll
-                    for (int q = 0; q < QG; q++) Pw[q] = src[q * 32];
-                    ccount++;
+                    for (int q = 0; q < QG; q++) Pw[q] = *reinterpret_cast<const uint4*>(rd + q * 512);
+                    rd += GB;
+                    if (rd >= ring_end) rd -= (size_t)D * GB;
                     __syncwarp();
                     issue();  // refill the slot just read
                     const uint32_t* wv = reinterpret_cast<const uint32_t*>(Pw);
                     const uint32_t* qrow = qx + (size_t)j * TG * K * G;
 #pragma unroll
                     for (int tt = 0; tt < TG; tt++) {
-                        if (TG == 1 || j * TG + tt < a.L) {
+                        if (TG == 1 || tt == 0 || j * TG + tt < a.L) {
                             uint32_t m[G];
 #pragma unroll
                             for (int g = 0; g < G; g++) m[g] = 0xffffffffu;

@@ -144,17 +144,29 @@ def make_unit(wl: Workload, b: int, h: int, n: int | None = None) -> Tuple[np.nd
     return bf16_bits_from_f32(k), bf16_bits_from_f32(v), bf16_bits_from_f32(q.astype(np.float32))
 
 
-def make_batch(wl: Workload, n: int | None = None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
-    """Whole workload: k, v uint16 [B][Hkv][n][d]; q uint16 [B][Hq][d]."""
+def make_batch(wl: Workload, n: int | None = None, threads: int = 1,
+               b0: int = 0) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Whole workload: k, v uint16 [B][Hkv][n][d]; q uint16 [B][Hq][d] (sequences b0 .. b0+B-1).
+    Units are independent streams, so threads > 1 gives identical arrays."""
     n = wl.n if n is None else n
     k = np.empty((wl.B, wl.Hkv, n, wl.d), dtype=np.uint16)
     v = np.empty_like(k)
     q = np.empty((wl.B, wl.Hq, wl.d), dtype=np.uint16)
-    for b in range(wl.B):
-        for h in range(wl.Hkv):
-            ku, vu, qu = make_unit(wl, b, h, n)
-            k[b, h], v[b, h] = ku, vu
-            q[b, h * wl.G:(h + 1) * wl.G] = qu
+
+    def one(bh):
+        b, h = bh
+        ku, vu, qu = make_unit(wl, b0 + b, h, n)
+        k[b, h], v[b, h] = ku, vu
+        q[b, h * wl.G:(h + 1) * wl.G] = qu
+
+    units = [(b, h) for b in range(wl.B) for h in range(wl.Hkv)]
+    if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, units))
+    else:
+        for bh in units:
+            one(bh)
     return k, v, q
 
 

@@ -27,7 +27,8 @@ KEYS = {
     "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pct",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pct",
 }
-UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+              "ns": 1, "us": 1e3, "ms": 1e6, "KB": 1e3, "MB": 1e6, "GB": 1e9, "B": 1}
 
 
 def raw(rep):
@@ -94,7 +95,8 @@ def main():
     os.makedirs("profiles", exist_ok=True)
     s = summarize(rep)
     L = launches(lcsv)
-    decode = next((v for k, v in s.items() if "decode_kernel" in k), None)
+    decode = next((v for k, v in s.items() if "decode5_kernel" in k), None) or \
+        next((v for k, v in s.items() if "decode_kernel" in k), None)
     out = {"tag": tag, "kernels": s, "launch_list": L,
            "decode": {"dram_bytes_per_launch": decode.get("dram_bytes_per_launch")} if decode else {}}
     with open("profiles/ncu_summary.json", "w") as f:

@@ -343,7 +343,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
         DecodeArgs t = a;
         v5 = decode5_layout(t, (int)G, max_smem_optin()) != 0;
     }
-    const int64_t tiles = B * Hkv * (g.nchunks + a.nstatic);
+    const int64_t tiles = B * Hkv * (g.nchunks * (v5 ? decode5_halves(a, num_sms()) : 1) + a.nstatic);
     const int64_t grid = v5 ? (tiles < num_sms() ? tiles : num_sms()) : tiles * a.tsplit;
     if (grid_out) *grid_out = grid;
     if (timeline) {

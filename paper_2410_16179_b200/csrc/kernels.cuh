@@ -48,6 +48,7 @@ struct DecodeArgs {
     // persistent kernel (decode5.cu): ring slots, shared-memory offsets, tile count
     int v5_ns, v5_off_qx, v5_off_qbw, v5_off_part, v5_off_rows, v5_off_xt, v5_off_fixed, v5_off_bars;
     int64_t v5_tiles;
+    int v5_hs;                        // chunk tiles per 1024-key chunk (1 or 2)
     int dbg;                          // debug flags (kernel 5: bit 0 = no L2 prefetch)
     unsigned long long* timeline;  // debug: [grid][16] globaltimer stamps, or NULL
     float* out;
@@ -62,6 +63,7 @@ struct DecodeArgs {
 int launch_decode(const DecodeArgs& a, cudaStream_t st);
 size_t decode5_layout(DecodeArgs& a, int G, int max_smem);
 int launch_decode5(const DecodeArgs& a, int nsm, int max_smem, cudaStream_t st);
+int decode5_halves(const DecodeArgs& a, int nsm);
 int launch_merge(const float* parts, int P, int64_t BH, float* out, cudaStream_t st);
 int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st);
 

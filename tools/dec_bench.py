@@ -98,6 +98,8 @@ if __name__ == "__main__":
         key, val = a.split("=")
         if key == "reps":
             R = int(val)
+        elif key == "kernel":
+            B_.set_decode_kernel(int(val))
         else:
             kw[key] = int(val)
     run(name, R=R, **kw)

@@ -376,17 +376,15 @@ def run_ours(args):
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     tr = _traffic("decode")
 
-    # ---- end to end through the public API: pinned host q in, host out back, every step
-    qh = [torch.from_numpy(q.view(np.int16)).view(torch.bfloat16).pin_memory() for _ in range(R)]
-    oh = [torch.empty((Bn, Hq, 128), dtype=torch.float32).pin_memory() for _ in range(R)]
-    qd = [torch.empty_like(tq) for _ in range(R)]
+    # ---- end to end through the public serving API (pkg.session: one CUDA graph per step holding the
+    # H2D copy of q from pinned host memory, encode, decode and the D2H copy of the output)
+    sess = [pkg.session(mps[r], ks[r], vs[r], Hq) for r in range(R)]
+    for s_ in sess:
+        s_.q_host.copy_(torch.from_numpy(q.view(np.int16)).view(torch.bfloat16))
     E = min(args.steps, args.e2e_steps)
 
     def e2e_step(i):
-        r = i % R
-        qd[r].copy_(qh[r], non_blocking=True)
-        mps[r].decode(qd[r], ks[r], vs[r], out=outs[r])
-        oh[r].copy_(outs[r], non_blocking=True)
+        sess[i % R].step()
 
     for i in range(max(args.warmup, R)):
         e2e_step(i)
@@ -406,8 +404,10 @@ def run_ours(args):
         e2e_ms = float(t.item())
     e2e_value = world * Bn / (e2e_ms / 1e3)
 
-    # correctness guard on the timed path: the last outputs are finite
+    # correctness guard on the timed paths: the last outputs are finite and the session's host output
+    # equals the device-timed path's output for the same inputs
     assert torch.isfinite(outs[0]).all().item(), "non-finite output"
+    assert torch.equal(sess[0].out_host, outs[0].cpu()), "session output differs from decode output"
 
     sweep = None
     if rank == 0 and args.sweep:

@@ -7,6 +7,6 @@ sequences build/decode (and the sharded variants over torch.distributed).
 """
 from . import binding
 from .binding import make_config, MagicPIGError
-from .index import MagicPIG
+from .index import DecodeSession, MagicPIG, session
 
-__all__ = ["binding", "make_config", "MagicPIG", "MagicPIGError"]
+__all__ = ["binding", "make_config", "MagicPIG", "MagicPIGError", "DecodeSession", "session"]

@@ -136,3 +136,45 @@ class MagicPIG:
     def status(self, which="decode") -> int:
         ws = self._ws_dec if which == "decode" else self._ws_build
         return B_.workspace_status(ws) if ws is not None else 0
+
+
+class DecodeSession:
+    """A serving step as ONE CUDA graph (CUDA graphs instead of a tracing compiler): the H2D copy of
+    q from a pinned host buffer, the query encode, the decode kernel and the D2H copy of the output
+    into a pinned host buffer.  ``step()`` replays it asynchronously on the current stream; write the
+    next query into ``q_host`` and read the result from ``out_host`` after synchronising.  The graph
+    binds this index, k and v: rebuild the session if they change."""
+
+    def __init__(self, mp: MagicPIG, k: torch.Tensor, v: torch.Tensor, Hq: int):
+        Bn, Hkv, n, _ = k.shape
+        dev = k.device
+        self.q_host = torch.zeros((Bn, Hq, 128), dtype=torch.bfloat16).pin_memory()
+        self.out_host = torch.zeros((Bn, Hq, 128), dtype=torch.float32).pin_memory()
+        self.q_dev = torch.zeros((Bn, Hq, 128), dtype=torch.bfloat16, device=dev)
+        self.out_dev = torch.zeros((Bn, Hq, 128), dtype=torch.float32, device=dev)
+        mp.decode_workspace(Bn, Hq, Hkv, n, dev)
+        self._mp, self._k, self._v = mp, k, v
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up outside the capture (library attributes, allocations)
+            self._body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+        torch.cuda.synchronize(dev)
+
+    def _body(self):
+        self.q_dev.copy_(self.q_host, non_blocking=True)
+        self._mp.decode(self.q_dev, self._k, self._v, out=self.out_dev)
+        self.out_host.copy_(self.out_dev, non_blocking=True)
+
+    def step(self):
+        self.graph.replay()
+        return self.out_host
+
+
+def session(mp: MagicPIG, k: torch.Tensor, v: torch.Tensor, Hq: int) -> DecodeSession:
+    """Graph-captured decode step for serving (see DecodeSession)."""
+    return DecodeSession(mp, k, v, Hq)

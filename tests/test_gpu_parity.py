@@ -341,3 +341,22 @@ def test_query_codes_near_zero_dots():
     assert pkg.binding.workspace_status(ws) == 0
     for h in range(3):
         np.testing.assert_array_equal(got[0, h], oracle.encode_query(bf(q[0, h]), W, K, L, 0))
+
+
+def test_decode_session_graph_matches_decode():
+    """The serving API (one CUDA graph: H2D q, encode, decode, D2H out) returns the same bits as the
+    eager decode, for two different queries replayed through the same graph."""
+    pkg = _pkg()
+    wl = synth.Workload("session", 950, B=1, Hq=8, Hkv=2, n=3000, K=10, L=150)
+    k, v, q = synth.make_batch(wl)
+    W = synth.make_projections(wl.K, wl.L, wl.mips)
+    tk, tv = _bf(k), _bf(v)
+    mp = pkg.MagicPIG(torch.from_numpy(W).to(_dev()), K=wl.K, L=wl.L).build(tk)
+    sess = pkg.session(mp, tk, tv, wl.Hq)
+    for qq in (q, q[:, ::-1].copy()):
+        tq = _bf(qq)
+        ref = mp.decode(tq, tk, tv).cpu()
+        sess.q_host.copy_(tq.cpu())
+        got = sess.step()
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref)

@@ -179,6 +179,37 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
                             float* partial, int32_t* s_count, uint32_t* s_mask, void* ws,
                             size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------ bucketed tables ---
+ * The paper's hash tables HT as inverted lists (
+ * SURVEY 8(f) NEXT-1): per (sequence, kv head) unit and table t, the key ids
+ * of this shard sorted by their K-bit code.  Query(HT, q_code) then reads only
+ * the L buckets each query head falls into instead of every key's codes; the
+ * sampled sets S_g are identical to the dense scan's (a key lies in exactly one
+ * bucket per table, so "in the query's bucket of >= min_collisions tables" is
+ * the P:84 rule).  Requires K <= 14 and ceil(n_local/32)*8 <= 200 KiB.
+ * Layout, int32 words: tables[B*Hkv][ L*(2^K+1) offsets | L*n_local ids ]:
+ *   offsets[t][c] .. offsets[t][c+1]  = the range of ids[t][] with code c
+ *   ids[t][e]                         = local key index (ascending within a
+ *                                       bucket is NOT guaranteed)
+ * magicpig_bucket_tables_words: size of `tables` (0 if unsupported). [host]
+ * magicpig_build_buckets: builds them from the packed codes of
+ *   magicpig_build_tables (call after it, same shapes).
+ * magicpig_decode_buckets[_encoded]: magicpig_decode[_encoded] with S from the
+ *   buckets; same arguments and outputs except `tables` replaces `codes`. */
+size_t magicpig_bucket_tables_words(const magicpig_config* cfg, int64_t B, int64_t Hkv, int64_t n_local);
+int magicpig_build_buckets(const magicpig_config* cfg, const uint32_t* codes, int64_t B, int64_t Hkv,
+                           int64_t n_local, int32_t* tables, void* stream);
+int magicpig_decode_buckets(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const int32_t* tables,
+                            const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v,
+                            int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global,
+                            const float* W, float* out, float* partial, int32_t* s_count, uint32_t* s_mask,
+                            void* ws, size_t ws_bytes, void* stream);
+int magicpig_decode_buckets_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                    const int32_t* tables, const float* center, const float* key_norm,
+                                    const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local,
+                                    int64_t seq_offset, int64_t n_global, float* out, float* partial,
+                                    int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes, void* stream);
+
 /* Log-sum-exp merge of P partial states ("recursive attention"):
  *   parts[P][BH][130] -> out[BH][128] = sum_j a_j e^{m_j-M} / sum_j s_j e^{m_j-M}
  * (fixed order j = 0..P-1, so every rank gets bit-identical results). */

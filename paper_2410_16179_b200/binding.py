@@ -54,6 +54,12 @@ _SIGS = {
     "magicpig_decode_encoded": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p,
                                  _p, _sz, _p], _i),
     "magicpig_merge_partials": ([_p, _i, _i64, _p, _p], _i),
+    "magicpig_bucket_tables_words": ([_p, _i64, _i64, _i64], _sz),
+    "magicpig_build_buckets": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
+    "magicpig_decode_buckets": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p,
+                                 _p, _p, _sz, _p], _i),
+    "magicpig_decode_buckets_encoded": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p,
+                                         _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_set_decode_kernel": ([_i], _i),
     "magicpig_export_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
     "magicpig_import_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
@@ -188,6 +194,34 @@ def decode(cfg, q, codes, center, key_norm, k, v, seq_offset, n_global, W, ws, o
     _check(lib().magicpig_decode(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(key_norm), _ptr(k), _ptr(v),
                                  B, Hkv, n, seq_offset, n_global, _ptr(W), _ptr(out), _ptr(partial),
                                  _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(), _stream()), "decode")
+
+
+def bucket_tables_words(cfg, B, Hkv, n) -> int:
+    return int(lib().magicpig_bucket_tables_words(_cfg(cfg), B, Hkv, n))
+
+
+def build_buckets(cfg, codes, B, Hkv, n, tables):
+    _check(lib().magicpig_build_buckets(_cfg(cfg), _ptr(codes), B, Hkv, n, _ptr(tables), _stream()), "build_buckets")
+
+
+def decode_buckets(cfg, q, tables, center, key_norm, k, v, seq_offset, n_global, W, ws, out=None, partial=None,
+                   s_count=None, s_mask=None):
+    B, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    _check(lib().magicpig_decode_buckets(_cfg(cfg), _ptr(q), Hq, _ptr(tables), _ptr(center), _ptr(key_norm), _ptr(k),
+                                         _ptr(v), B, Hkv, n, seq_offset, n_global, _ptr(W), _ptr(out), _ptr(partial),
+                                         _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(), _stream()),
+           "decode_buckets")
+
+
+def decode_buckets_encoded(cfg, q, tables, center, key_norm, k, v, seq_offset, n_global, ws, out=None,
+                           partial=None, s_count=None, s_mask=None):
+    B, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    _check(lib().magicpig_decode_buckets_encoded(_cfg(cfg), _ptr(q), Hq, _ptr(tables), _ptr(center), _ptr(key_norm),
+                                                 _ptr(k), _ptr(v), B, Hkv, n, seq_offset, n_global, _ptr(out),
+                                                 _ptr(partial), _ptr(s_count), _ptr(s_mask), _ptr(ws), ws.numel(),
+                                                 _stream()), "decode_buckets_encoded")
 
 
 def encode_queries(cfg, q, W, ws):

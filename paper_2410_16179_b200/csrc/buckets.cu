@@ -1,0 +1,234 @@
+// buckets.cu -- the paper's hash tables HT as inverted lists:
+// for every (sequence, kv head) unit and table t, the keys sorted by their K-bit
+// code, so that Query(HT, q_code) (Alg. 1) reads only the L buckets
+// the query falls into ("negligible computationally", P:446-456
+// table sizes) instead of streaming every key's codes.
+//
+//   bucket_build_kernel  CTA per (unit, table): codes of the table from the bit
+//                        planes -> shared-memory histogram over 2^K buckets ->
+//                        exclusive scan -> offsets; scatter of key ids.
+//   bucket_mark_kernel   CTA per (unit, query head): for each table the ids of
+//                        the query's bucket -> two shared-memory bitmaps
+//                        (seen >= 1, seen >= 2; a key is in exactly one bucket
+//                        per table, so "seen twice" = matched in >= 2 tables,
+//                        the P:84 rule) -> S bitmap in global memory, consumed
+//                        by the decode kernel in place of the code scan.
+// S is the same set as the dense scan computes (oracle pin P10 proves the two
+// forms equal in the oracle; the GPU parity tests check both against it).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mp {
+
+constexpr int BK_THREADS = 512;
+constexpr int BM_THREADS = 512;
+
+// code of table t for the 32 keys of block blk (bit r of word b = column t*K+b of key 32*blk+r)
+__device__ __forceinline__ void table_words(const uint32_t* __restrict__ cu, int KLq, int K, int t, int64_t blk,
+                                            uint32_t (&w)[16]) {
+    const int64_t chunk = blk >> 5, l = blk & 31;
+#pragma unroll
+    for (int b = 0; b < 16; b++) {
+        if (b < K) {
+            const int col = t * K + b;
+            w[b] = __ldg(cu + ((chunk * KLq + (col >> 2)) * 32 + l) * 4 + (col & 3));
+        }
+    }
+}
+__device__ __forceinline__ uint32_t key_code(const uint32_t (&w)[16], int K, int r) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int b = 0; b < 16; b++)
+        if (b < K) c |= ((w[b] >> r) & 1u) << b;
+    return c;
+}
+
+// block-wide exclusive scan of hist[0..nb) in place; returns the total (all threads)
+__device__ int block_exclusive_scan(int* hist, int nb, int* warp_tot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+    const int per = (nb + nt - 1) / nt, b0 = min(nb, tid * per), b1 = min(nb, b0 + per);
+    int s = 0;
+    for (int b = b0; b < b1; b++) s += hist[b];
+    int incl = s;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, m);
+        if (lane >= m) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = nt >> 5;
+        int v = lane < nw ? warp_tot[lane] : 0, iv = v;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, iv, m);
+            if (lane >= m) iv += u;
+        }
+        if (lane < nw) warp_tot[lane] = iv - v;
+        if (lane == 31) warp_tot[32] = iv;
+    }
+    __syncthreads();
+    int run = warp_tot[warp] + incl - s;
+    for (int b = b0; b < b1; b++) {
+        const int h = hist[b];
+        hist[b] = run;
+        run += h;
+    }
+    const int total = warp_tot[32];
+    __syncthreads();
+    return total;
+}
+
+// grid (L, units); dynamic smem = 2^K ints
+__global__ void __launch_bounds__(BK_THREADS) bucket_build_kernel(const uint32_t* __restrict__ codes, int64_t n_local,
+                                                                   int K, int L, int KLq, int64_t nchunks,
+                                                                   int32_t* __restrict__ tables) {
+    extern __shared__ int hist[];
+    __shared__ int warp_tot[33];
+    const int t = blockIdx.x;
+    const int64_t u = blockIdx.y;
+    const int nb = 1 << K;
+    const uint32_t* cu = codes + (size_t)u * nchunks * KLq * 128;
+    int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    int32_t* offs = tu + (size_t)t * (nb + 1);
+    int32_t* ids = tu + (size_t)L * (nb + 1) + (size_t)t * n_local;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int64_t nblk = (n_local + 31) >> 5;
+    for (int64_t blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
+        uint32_t w[16];
+        table_words(cu, KLq, K, t, blk, w);
+        const int nr = (int)min((int64_t)32, n_local - blk * 32);
+        for (int r = 0; r < nr; r++) atomicAdd(&hist[key_code(w, K, r)], 1);
+    }
+    __syncthreads();
+    const int total = block_exclusive_scan(hist, nb, warp_tot);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) offs[b] = hist[b];
+    if (threadIdx.x == 0) offs[nb] = total;
+    __syncthreads();
+    for (int64_t blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
+        uint32_t w[16];
+        table_words(cu, KLq, K, t, blk, w);
+        const int nr = (int)min((int64_t)32, n_local - blk * 32);
+        for (int r = 0; r < nr; r++) {
+            const int pos = atomicAdd(&hist[key_code(w, K, r)], 1);
+            ids[pos] = (int32_t)(blk * 32 + r);
+        }
+    }
+}
+
+// grid (Hq, B); dynamic smem = 2 * nw words + 2 * (L + 1) ints.  qbits [B][Hq][KLw] (bit j = column j of q_g).
+// Latency structure: one round for every table's bucket range (thread per table), a block scan of the
+// bucket sizes, then all ids of all buckets flattened over the CTA (each thread's loads independent).
+__global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t* __restrict__ qbits,
+                                                                  const int32_t* __restrict__ tables, int64_t Hq,
+                                                                  int64_t Hkv, int64_t n_local, int K, int L, int KLw,
+                                                                  int minc, uint32_t* __restrict__ sbits) {
+    extern __shared__ uint32_t seen[];  // seen1[nw], seen2[nw], lo[L], start[L + 1]
+    __shared__ int warp_tot[33];
+    const int64_t hq = blockIdx.x, b = blockIdx.y;
+    const int64_t G = Hq / Hkv, u = b * Hkv + hq / G;
+    const int nb = 1 << K;
+    const int64_t nw = (n_local + 31) >> 5;
+    uint32_t* seen1 = seen;
+    uint32_t* seen2 = seen + nw;
+    int* lo_s = reinterpret_cast<int*>(seen + 2 * nw);
+    int* start = lo_s + L;
+    const int tid = threadIdx.x;
+    const int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    for (int64_t w = tid; w < 2 * nw; w += blockDim.x) seen[w] = 0u;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
+    const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
+    for (int t = tid; t < L; t += blockDim.x) {
+        // query code of table t: columns t*K .. t*K+K-1 (little endian, R7)
+        const int c0 = t * K;
+        const uint64_t two = (uint64_t)__ldcg(qb + (c0 >> 5)) |
+                             ((c0 >> 5) + 1 < KLw ? (uint64_t)__ldcg(qb + (c0 >> 5) + 1) << 32 : 0ull);
+        const int qc = (int)((two >> (c0 & 31)) & (uint64_t)(nb - 1));
+        const int32_t* offs = tu + (size_t)t * (nb + 1);
+        const int lo = __ldg(offs + qc), hi = __ldg(offs + qc + 1);
+        lo_s[t] = lo;
+        start[t] = hi - lo;
+    }
+    __syncthreads();
+    const int total = block_exclusive_scan(start, L, warp_tot);  // start[t] = first flat index of table t
+    if (tid == 0) start[L] = total;
+    __syncthreads();
+    const int32_t* ids0 = tu + (size_t)L * (nb + 1);
+    constexpr int ILP = 8;
+    for (int e0 = tid; e0 < total; e0 += blockDim.x * ILP) {
+        int ids[ILP];
+#pragma unroll
+        for (int j = 0; j < ILP; j++) {
+            const int e = e0 + j * blockDim.x;
+            ids[j] = -1;
+            if (e < total) {
+                int lo = 0, hi = L;  // table of flat index e: last t with start[t] <= e
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (start[mid] <= e) lo = mid;
+                    else hi = mid;
+                }
+                ids[j] = __ldg(ids0 + (size_t)lo * n_local + lo_s[lo] + (e - start[lo]));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < ILP; j++) {
+            if (ids[j] >= 0) {
+                const int i = ids[j];
+                const uint32_t bit = 1u << (i & 31);
+                const uint32_t old = atomicOr(&seen1[i >> 5], bit);
+                if (minc > 1 && (old & bit)) atomicOr(&seen2[i >> 5], bit);
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t* src = minc > 1 ? seen2 : seen1;
+    uint32_t* dst = sbits + (b * Hq + hq) * nw;
+    for (int64_t w = tid; w < nw; w += blockDim.x) dst[w] = src[w];
+}
+
+size_t bucket_tables_words(int K, int L, int64_t units, int64_t n_local) {
+    return (size_t)units * L * (((size_t)1 << K) + 1 + (size_t)n_local);
+}
+
+int launch_bucket_build(const uint32_t* codes, int64_t units, int64_t n_local, int K, int L, int KLq,
+                        int64_t nchunks, int32_t* tables, cudaStream_t st) {
+    if (units < 1 || n_local < 1) return 0;
+    const size_t smem = ((size_t)1 << K) * 4;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(bucket_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+        return MAGICPIG_ECUDA;
+    bucket_build_kernel<<<dim3((unsigned)L, (unsigned)units), BK_THREADS, smem, st>>>(codes, n_local, K, L, KLq,
+                                                                                     nchunks, tables);
+    count_launch(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, int64_t Hq, int64_t Hkv,
+                       int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st) {
+    const size_t smem = (size_t)((n_local + 31) >> 5) * 8 + (size_t)(2 * L + 1) * 4;
+    if (smem > 208 * 1024) return MAGICPIG_EINVAL;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(bucket_mark_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+        return MAGICPIG_ECUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)Hq, (unsigned)B);
+    cfg.blockDim = dim3(BM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, bucket_mark_kernel, qbits, tables, Hq, Hkv, n_local, K, L, KLw, minc,
+                                       sbits);
+    count_launch(1);
+    return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+}  // namespace mp

@@ -50,6 +50,11 @@ static bool cfg_ok(const magicpig_config* c) {
     return true;
 }
 
+// bucketed tables: 2^K-entry histogram in shared memory, n-bit seen bitmaps per head in shared memory
+static bool buckets_ok(const magicpig_config* c, int64_t n_local) {
+    return cfg_ok(c) && c->K <= 14 && (size_t)((n_local + 31) / 32) * 8 <= 200 * 1024;
+}
+
 static bool shape_ok(int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global) {
     if (B < 1 || Hkv < 1 || n_local < 0 || seq_offset < 0) return false;
     if (seq_offset + n_local > n_global) return false;
@@ -119,6 +124,7 @@ struct DecodeWs {
     uint32_t* unit_ctr;
     float* parts;
     int32_t* chunk_cnt;
+    uint32_t* sbits;
     size_t bytes;
 };
 
@@ -146,6 +152,7 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     const size_t parts5 = (size_t)(units + num_sms()) * G * PREC5 * 4;         // record u + CTA
     w.parts = (float*)take(parts4 > parts5 ? parts4 : parts5);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
+    w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4);  // bucket mode S bitmaps
     w.bytes = off;
     return w;
 }
@@ -261,14 +268,16 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
                        const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B,
                        int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
                        float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
-                       void* stream, unsigned long long* timeline, int64_t timeline_len, int64_t* grid_out) {
+                       void* stream, unsigned long long* timeline, int64_t timeline_len, int64_t* grid_out,
+                       const int32_t* tables = nullptr) {
     if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
     if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
     const int64_t G = Hq / Hkv;
     if (G != 1 && G != 2 && G != 4 && G != 8) return MAGICPIG_EINVAL;
     if (!q || !center || !ws) return MAGICPIG_EINVAL;
     if (n_local > 0 && !key_norm) return MAGICPIG_EINVAL;
-    if (n_local > 0 && (!codes || !k || !v)) return MAGICPIG_EINVAL;
+    if (n_local > 0 && ((!codes && !tables) || !k || !v)) return MAGICPIG_EINVAL;
+    if (tables && !buckets_ok(cfg, n_local)) return MAGICPIG_EINVAL;
     DecodeWs w = decode_layout(cfg, B, Hq, Hkv, n_local, ws);
     if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
     cudaStream_t st = S(stream);
@@ -337,11 +346,18 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
     const int kver = g_decode_kernel.load();
-    bool v5 = kver % 10 == 5;
+    bool v5 = kver % 10 == 5 || tables;  // bucket mode runs on the persistent kernel only
     a.dbg = kver / 10;
     if (v5) {
         DecodeArgs t = a;
         v5 = decode5_layout(t, (int)G, max_smem_optin()) != 0;
+        if (!v5 && tables) return MAGICPIG_EINVAL;
+    }
+    if (tables) {  // Query(HT, q_code) on the bucketed tables -> S bitmaps (PDL after the encode)
+        int rc = launch_bucket_mark(w.qbits, tables, B, Hq, Hkv, n_local, cfg->K, cfg->L, g.KLw,
+                                    cfg->min_collisions, w.sbits, st);
+        if (rc) return rc;
+        a.sbits = w.sbits;
     }
     const int64_t tiles = B * Hkv * (g.nchunks * (v5 ? decode5_halves(a, num_sms()) : 1) + a.nstatic);
     const int64_t grid = v5 ? (tiles < num_sms() ? tiles : num_sms()) : tiles * a.tsplit;
@@ -395,6 +411,42 @@ int magicpig_decode(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, c
     }
     return magicpig_decode_encoded(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
                                    partial, s_count, s_mask, ws, ws_bytes, stream);
+}
+
+size_t magicpig_bucket_tables_words(const magicpig_config* cfg, int64_t B, int64_t Hkv, int64_t n_local) {
+    if (!buckets_ok(cfg, n_local) || B < 1 || Hkv < 1 || n_local < 0) return 0;
+    return bucket_tables_words(cfg->K, cfg->L, B * Hkv, n_local);
+}
+
+int magicpig_build_buckets(const magicpig_config* cfg, const uint32_t* codes, int64_t B, int64_t Hkv,
+                           int64_t n_local, int32_t* tables, void* stream) {
+    if (!buckets_ok(cfg, n_local) || B < 1 || Hkv < 1 || n_local < 0 || !codes || !tables) return MAGICPIG_EINVAL;
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    return launch_bucket_build(codes, B * Hkv, n_local, cfg->K, cfg->L, g.KLq, g.nchunks, tables, S(stream));
+}
+
+int magicpig_decode_buckets(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const int32_t* tables,
+                            const float* center, const float* key_norm, const uint16_t* k, const uint16_t* v,
+                            int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global,
+                            const float* W, float* out, float* partial, int32_t* s_count, uint32_t* s_mask,
+                            void* ws, size_t ws_bytes, void* stream) {
+    if (!W || (n_local > 0 && !tables)) return MAGICPIG_EINVAL;
+    if (n_local > 0) {
+        int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
+        if (rc) return rc;
+    }
+    return decode_impl(cfg, q, Hq, nullptr, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
+                       partial, s_count, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables);
+}
+
+int magicpig_decode_buckets_encoded(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                    const int32_t* tables, const float* center, const float* key_norm,
+                                    const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local,
+                                    int64_t seq_offset, int64_t n_global, float* out, float* partial,
+                                    int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes, void* stream) {
+    if (n_local > 0 && !tables) return MAGICPIG_EINVAL;
+    return decode_impl(cfg, q, Hq, nullptr, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
+                       partial, s_count, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables);
 }
 
 int magicpig_merge_partials(const float* parts, int P, int64_t BH, float* out, void* stream) {

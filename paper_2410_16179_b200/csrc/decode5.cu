@@ -276,7 +276,10 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                              : "memory");
             }
         };
-        if (warp == 0 && !(a.dbg & 1))
+        // bucket mode (a.sbits != NULL): S comes from the bucketed hash-table query (buckets.cu) as
+        // per-head bitmaps; the scan warps only read them and compact (no code stream)
+        const bool dense = a.sbits == nullptr;
+        if (warp == 0 && !(a.dbg & 1) && dense)
             for (int64_t c = gc0; c < gc0 + PF_CHUNKS; c++) prefetch_chunk(c);
         // the ring is filled only after the query masks are built (from L2, where the prefetch put
         // the codes): a ring fill issued first queues ~100 KB of loads ahead of the query-code load
@@ -302,10 +305,11 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
             if (!is_static) {
                 const int64_t ct = r - a.nstatic, chunk = ct >> hsl;
                 const int64_t cbase = chunk * KCHUNK + (ct & hsl) * (LPG * 32);  // first key of the tile
-                if (warp == 0 && (a.dbg & 2) && (ct & hsl) == 0) {
+                if (warp == 0 && (a.dbg & 2) && (ct & hsl) == 0 && dense) {
                     const int64_t gc = u * a.nchunks + chunk + PF_CHUNKS;
                     if (gc >= gc0 + PF_CHUNKS) prefetch_chunk(gc);
                 }
+                if (dense) {
                 if (u != cur_u) {  // query masks of unit u: QX[c][g] = qbit ? 0 : ~0 (P ^ QX = 1 where bits agree)
                     bar_named(1, NSW * 32);
                     for (int e = tid; e < G * a.KLw; e += NSW * 32) qbw[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
@@ -390,6 +394,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                     s_part[((warp * G + g) * 2 + 0) * 32 + lane] = s1[g];
                     s_part[((warp * G + g) * 2 + 1) * 32 + lane] = s2[g];
                 }
+                }  // dense
                 if (tid < 32) {
                     const int64_t base = cbase + lane * 32;
                     f.s_tm[lane] = (range_mask(base, -a.seq_offset, (int64_t)a.sink - a.seq_offset) |
@@ -401,16 +406,24 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                 // warps -> CTA: (a1,a2)+(b1,b2) = (a1|b1, a2|b2|(a1&b1)); S_g = count >= minc on D
                 if (tid < G * 32) {
                     const int g = tid >> 5;
-                    uint32_t f1 = 0, f2 = 0;
+                    const int64_t nwb = (a.n_local + 31) >> 5;
+                    uint32_t sel;
+                    if (dense) {
+                        uint32_t f1 = 0, f2 = 0;
 #pragma unroll
-                    for (int w = 0; w < NSW; w++) {
-                        const uint32_t b1 = s_part[((w * G + g) * 2 + 0) * 32 + lane];
-                        const uint32_t b2 = s_part[((w * G + g) * 2 + 1) * 32 + lane];
-                        f2 |= b2 | (f1 & b1);
-                        f1 |= b1;
+                        for (int w = 0; w < NSW; w++) {
+                            const uint32_t b1 = s_part[((w * G + g) * 2 + 0) * 32 + lane];
+                            const uint32_t b2 = s_part[((w * G + g) * 2 + 1) * 32 + lane];
+                            f2 |= b2 | (f1 & b1);
+                            f1 |= b1;
+                        }
+                        sel = a.minc == 1 ? f1 : f2;
+                    } else {
+                        const int64_t wi = (cbase >> 5) + lane;
+                        sel = (lane < LPG && wi < nwb) ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
                     }
                     const int64_t base = cbase + lane * 32;
-                    uint32_t v = (a.minc == 1 ? f1 : f2) & range_mask(base, 0, a.n_local) & ~f.s_tm[lane];
+                    uint32_t v = sel & range_mask(base, 0, a.n_local) & ~f.s_tm[lane];
                     if (lane >= LPG) v = 0u;
                     f.s_sel[g][lane] = v;
                     int cnt = __popc(v);
@@ -644,6 +657,31 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
     int di = 0;
     bool first_batch = true;
     long long acc_df = 0, acc_rw = 0;
+    // row staging runs ahead of the compute over a flat (descriptor, batch) sequence: batches are staged
+    // up to NSTAGE - 1 ahead of the one being computed.  In bucket mode (descriptors arrive faster than
+    // they are gathered) the cursor also crosses into the next descriptor, so its first rows are in
+    // flight while the current one finishes; in dense mode it stops at the descriptor boundary.
+    const bool cross = a.sbits != nullptr;
+    const int ndesc = (int)(t1 - t0);
+    int sdi = 0, sbt = 0;  // next (descriptor, batch) to stage
+    uint32_t cseq = 0;     // batches computed so far (= stage buffer sequence)
+    auto stage_upto = [&](uint32_t limit) {
+        // at most one descriptor ahead: descriptor di + 2 reuses the slot of di, which is released only
+        // after di is computed (waiting for it here would deadlock)
+        while (rseq < limit && sdi < ndesc && sdi <= di + (cross ? 1 : 0)) {
+            if (sdi > di) mbar_wait(&f.dfull[sdi & 1], (uint32_t)((sdi >> 1) & 1));
+            const Desc& Ds = f.desc[sdi & 1];
+            const int nbs = (Ds.n + RB - 1) / RB;
+            if (sbt < nbs) {
+                stage(Ds, sbt * RB, min(RB, Ds.n - sbt * RB), Ds.unit);
+                sbt++;
+            }
+            if (sbt >= nbs) {
+                sdi++;
+                sbt = 0;
+            }
+        }
+    };
     if (t0 < t1) {  // the first unit's data while the scan warps work
         cur_u = t0 / tpu;
         load_unit(cur_u);
@@ -665,11 +703,10 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
         if (gtid < G) f.cnt[gtid] += (float)D.cnt[gtid];
         const int n = D.n;
         const int nbatch = (n + RB - 1) / RB;
-        const uint32_t rbase = rseq;
-        for (int bt = 0; bt < 2 && bt < nbatch; bt++) stage(D, bt * RB, min(RB, n - bt * RB), u);
+        if (nbatch == 0 && sdi == di) sdi++, sbt = 0;  // nothing to stage for an empty descriptor
         for (int bt = 0; bt < nbatch; bt++) {
-            if (bt + 2 < nbatch) stage(D, (bt + 2) * RB, min(RB, n - (bt + 2) * RB), u);
-            const uint32_t k = rbase + bt;
+            stage_upto(cseq + NSTAGE);
+            const uint32_t k = cseq++;
             const uint8_t* buf = rows + (size_t)(k % NSTAGE) * RB * ROWB;
             long long tr0 = clock64();
             if (a.dbg & 8) mbar_wait_sleep(&f.rowbar[k % NSTAGE], (k / NSTAGE) & 1);

@@ -55,6 +55,7 @@ struct DecodeArgs {
     float* partial;
     int32_t* s_count;
     uint32_t* s_mask;
+    const uint32_t* sbits;           // bucket mode: S bitmaps [B][Hq][ceil(n/32)] (NULL = dense scan)
     uint32_t* unit_ctr;
     float* parts;
     int32_t* chunk_cnt;
@@ -63,6 +64,11 @@ struct DecodeArgs {
 int launch_decode(const DecodeArgs& a, cudaStream_t st);
 size_t decode5_layout(DecodeArgs& a, int G, int max_smem);
 int launch_decode5(const DecodeArgs& a, int nsm, int max_smem, cudaStream_t st);
+size_t bucket_tables_words(int K, int L, int64_t units, int64_t n_local);
+int launch_bucket_build(const uint32_t* codes, int64_t units, int64_t n_local, int K, int L, int KLq,
+                        int64_t nchunks, int32_t* tables, cudaStream_t st);
+int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, int64_t Hq, int64_t Hkv,
+                       int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st);
 int decode5_halves(const DecodeArgs& a, int nsm);
 int launch_merge(const float* parts, int P, int64_t BH, float* out, cudaStream_t st);
 int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st);

@@ -30,13 +30,18 @@ class IndexBuffers:
     key_norm: torch.Tensor  # [B][Hkv][n] f32 |xbar_i|
     key_sum: torch.Tensor  # [B][Hkv][128][2] int64 (q64)
     count: torch.Tensor    # [B][Hkv] int64
+    tables: Optional[torch.Tensor] = None  # bucketed hash tables (int32 words), when buckets=True
 
 
 class MagicPIG:
     """One attention layer's LSH index over a KV cache k, v [B][Hkv][n][128] bf16."""
 
-    def __init__(self, W: torch.Tensor, K=10, L=150, center=1, mips=1, min_collisions=2, sink=4, local=64):
+    def __init__(self, W: torch.Tensor, K=10, L=150, center=1, mips=1, min_collisions=2, sink=4, local=64,
+                 buckets=False):
+        """buckets=True also builds the paper's hash tables as inverted lists (per table, key ids sorted by
+        code) and decodes by reading only the query's buckets (same S as the dense code scan)."""
         self.cfg = B_.make_config(K, L, center, mips, min_collisions, sink, local)
+        self.buckets = bool(buckets)
         rc = B_.lib().magicpig_validate_config(B_.C.byref(self.cfg))
         if rc != 0:
             raise B_.MagicPIGError("unsupported configuration")
@@ -83,7 +88,18 @@ class MagicPIG:
         b = self.buf
         B_.build_index(self.cfg, k, self.W, b.center, b.r2, b.codes, b.key_norm, b.key_sum, b.count, self._ws_build)
         self.seq_offset, self.n_global, self.shape = 0, n, (Bn, Hkv, n)
+        self._build_buckets()
         return self
+
+    def _build_buckets(self):
+        if not self.buckets:
+            return
+        Bn, Hkv, n = self.shape
+        words = B_.bucket_tables_words(self.cfg, Bn, Hkv, n)
+        if words == 0:
+            raise B_.MagicPIGError("bucketed tables unsupported for this configuration (K <= 14, n <= 819200)")
+        self.buf.tables = torch.empty((words,), dtype=torch.int32, device=self.buf.codes.device)
+        B_.build_buckets(self.cfg, self.buf.codes, Bn, Hkv, n, self.buf.tables)
 
     def build_sharded(self, k_local: torch.Tensor, seq_offset: int, n_global: int, group=None):
         """Sequence-sharded build: this rank holds keys [seq_offset, seq_offset + n_local)."""
@@ -105,6 +121,7 @@ class MagicPIG:
         B_.reduce_stats(1, all_r2, None, P, Bn, Hkv, b.r2, None)
         B_.build_tables(self.cfg, k_local, seq_offset, n_global, self.W, b.center, b.r2, b.codes, b.key_norm, ws)
         self.seq_offset, self.n_global, self.shape = seq_offset, n_global, (Bn, Hkv, n)
+        self._build_buckets()
         return self
 
     # ------------------------------------------------------------ decode
@@ -117,8 +134,12 @@ class MagicPIG:
         if out is None and partial is None:
             out = torch.empty((Bn, Hq, 128), dtype=torch.float32, device=q.device)
         b = self.buf
-        B_.decode(self.cfg, q, b.codes, b.center, b.key_norm, k, v, self.seq_offset, self.n_global, self.W, ws,
-                  out=out, partial=partial, s_count=s_count, s_mask=s_mask)
+        if self.buckets:
+            B_.decode_buckets(self.cfg, q, b.tables, b.center, b.key_norm, k, v, self.seq_offset, self.n_global,
+                              self.W, ws, out=out, partial=partial, s_count=s_count, s_mask=s_mask)
+        else:
+            B_.decode(self.cfg, q, b.codes, b.center, b.key_norm, k, v, self.seq_offset, self.n_global, self.W, ws,
+                      out=out, partial=partial, s_count=s_count, s_mask=s_mask)
         return out if out is not None else partial
 
     def decode_sharded(self, q, k_local, v_local, group=None, out=None, s_count=None):

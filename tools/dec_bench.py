@@ -20,7 +20,7 @@ import paper_2410_16179_b200 as pkg  # noqa: E402
 from paper_2410_16179_b200 import binding as B_  # noqa: E402
 
 
-def run(name, R=4, G_STEPS=64, **over):
+def run(name, R=4, G_STEPS=64, buckets=0, **over):
     wl = dataclasses.replace(synth.CONFIGS[name], **over)
     dev = torch.device("cuda:0")
     k, v, q = synth.make_batch(wl)
@@ -32,7 +32,7 @@ def run(name, R=4, G_STEPS=64, **over):
     for r in range(R):
         kr = tk if r == 0 else tk.clone()
         vr = tv if r == 0 else tv.clone()
-        mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, mips=wl.mips).build(kr)
+        mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, mips=wl.mips, buckets=bool(buckets)).build(kr)
         mp.release_build_workspace()
         mps.append(mp), ks.append(kr), vs.append(vr)
     cfg = mps[0].cfg
@@ -42,8 +42,8 @@ def run(name, R=4, G_STEPS=64, **over):
     nw = (n + 31) // 32
     smask = torch.zeros((Bn, Hq, nw), dtype=torch.int32, device=dev)
     scount = torch.zeros((Bn, Hq), dtype=torch.int32, device=dev)
-    B_.decode(cfg, tq, mps[0].buf.codes, mps[0].buf.center, mps[0].buf.key_norm, ks[0], vs[0], 0, n, tW, ws,
-              out=out, s_count=scount, s_mask=smask)
+    mps[0]._ws_dec = ws
+    mps[0].decode(tq, ks[0], vs[0], out=out, s_count=scount, s_mask=smask)
     torch.cuda.synchronize()
     sm = smask.cpu().numpy().view(np.uint32).reshape(Bn, Hkv, wl.G, nw)
     union = np.bitwise_or.reduce(sm, axis=2)
@@ -54,8 +54,12 @@ def run(name, R=4, G_STEPS=64, **over):
         + Bn * Hkv * 512
 
     def kern(r):
-        B_.decode_encoded(cfg, tq, mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n, ws,
-                          out=out)
+        if buckets:
+            B_.decode_buckets_encoded(cfg, tq, mps[r].buf.tables, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r],
+                                      0, n, ws, out=out)
+        else:
+            B_.decode_encoded(cfg, tq, mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n,
+                              ws, out=out)
 
     def step(r):
         B_.encode_queries(cfg, tq, tW, ws)
@@ -82,7 +86,23 @@ def run(name, R=4, G_STEPS=64, **over):
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3 / G_STEPS)
         res[nm + "_us"] = float(np.median(ts))
-    res.update(config=name, n=n, B=Bn, K=wl.K, L=wl.L, alg_MB=alg / 1e6,
+    if buckets:  # codes term -> the ids of the query's buckets + offsets + S bitmaps (write + read)
+        qc = torch.zeros((Bn, Hq, wl.L), dtype=torch.int16, device=dev)
+        B_.query_codes(cfg, tq, tW, qc, ws)
+        qc = qc.cpu().numpy().view(np.uint16).astype(np.int64)
+        nb = 1 << wl.K
+        per = wl.L * (nb + 1 + n)
+        tabs = mps[0].buf.tables.cpu().numpy()
+        ids_read = 0
+        for b in range(Bn):
+            for hq in range(Hq):
+                u = b * Hkv + hq // wl.G
+                offs = tabs[u * per:u * per + wl.L * (nb + 1)].reshape(wl.L, nb + 1)
+                c = qc[b, hq]
+                ids_read += int((offs[np.arange(wl.L), c + 1] - offs[np.arange(wl.L), c]).sum())
+        alg = alg - Bn * Hkv * (n - nT) * KL / 8 + ids_read * 4 + Bn * Hq * wl.L * 8 + 2 * Bn * Hq * ((n + 31) // 32) * 4
+        res["ids_read"] = ids_read
+    res.update(config=name, n=n, B=Bn, K=wl.K, L=wl.L, alg_MB=alg / 1e6, buckets=buckets,
                sampled=float(scount.float().mean()) / max(n - nT, 1), union=n_union,
                GBs=alg / res["kernel_us"] / 1e3, frac=alg / res["kernel_us"] / 1e3 / 6545.0,
                status=B_.workspace_status(ws))
@@ -98,6 +118,8 @@ if __name__ == "__main__":
         key, val = a.split("=")
         if key == "reps":
             R = int(val)
+        elif key == "buckets":
+            kw["buckets"] = int(val)
         elif key == "kernel":
             B_.set_decode_kernel(int(val))
         else:

@@ -171,9 +171,12 @@ def cpu_oracle_timing(wl, k, v, q, W, steps_cap=None, target_s=10.0):
 
 
 # ----------------------------------------------------------------------------- context sweep
-def sweep_point(wl, dev, tW, peak, graph_launches=64):
+def sweep_point(wl, dev, tW, peak, graph_launches=64, buckets=False):
     """Decode kernel alone (the roofline kernel) at one workload: inputs rotated over R
-    replicas so that a launch's bytes were last touched R-1 launches earlier (> L2)."""
+    replicas so that a launch's bytes were last touched R-1 launches earlier (> L2).
+    buckets=True: the bucketed hash-table path (bucket query kernel + decode kernel in bitmap
+    mode); its algorithmic bytes replace the code stream by the ids of the query's buckets,
+    the bucket offsets and the S bitmaps (written and read)."""
     import torch
     import paper_2410_16179_b200 as pkg
     from paper_2410_16179_b200 import binding as B_
@@ -189,7 +192,7 @@ def sweep_point(wl, dev, tW, peak, graph_launches=64):
         kr = tk if r == 0 else tk.clone()
         vr = tv if r == 0 else tv.clone()
         mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, center=wl.center, mips=wl.mips, min_collisions=wl.min_collisions,
-                          sink=wl.sink, local=wl.local).build(kr)
+                          sink=wl.sink, local=wl.local, buckets=buckets).build(kr)
         mp.release_build_workspace()
         mps.append(mp), ks.append(kr), vs.append(vr)
     cfg = mps[0].cfg
@@ -199,8 +202,8 @@ def sweep_point(wl, dev, tW, peak, graph_launches=64):
     nw = (n + 31) // 32
     smask = torch.zeros((Bn, Hq, nw), dtype=torch.int32, device=dev)
     scount = torch.zeros((Bn, Hq), dtype=torch.int32, device=dev)
-    B_.decode(cfg, tq, mps[0].buf.codes, mps[0].buf.center, mps[0].buf.key_norm, ks[0], vs[0], 0, n, tW, ws,
-              out=out, s_count=scount, s_mask=smask)
+    mps[0]._ws_dec = ws
+    mps[0].decode(tq, ks[0], vs[0], out=out, s_count=scount, s_mask=smask)
     torch.cuda.synchronize()
     sm = smask.cpu().numpy().view(np.uint32).reshape(Bn, Hkv, wl.G, nw)
     n_union = int(np.unpackbits(np.bitwise_or.reduce(sm, axis=2).view(np.uint8)).sum())
@@ -209,9 +212,31 @@ def sweep_point(wl, dev, tW, peak, graph_launches=64):
     alg = (Bn * Hkv * (n - nT) * KL / 8 + (n_union + Bn * Hkv * nT) * 512 + n_union * 4 + Bn * Hq * (256 + KL / 8)
            + Bn * Hkv * 512)
 
+    ids_read = None
+    if buckets:
+        qc = torch.zeros((Bn, Hq, wl.L), dtype=torch.int16, device=dev)
+        B_.query_codes(cfg, tq, tW, qc, ws)
+        qc = qc.cpu().numpy().view(np.uint16).astype(np.int64)
+        nb = 1 << wl.K
+        per = wl.L * (nb + 1 + n)
+        tabs = mps[0].buf.tables
+        ids_read = 0
+        for b in range(Bn):
+            for hq in range(Hq):
+                u = b * Hkv + hq // wl.G
+                offs = tabs[u * per:u * per + wl.L * (nb + 1)].view(wl.L, nb + 1).cpu().numpy()
+                c = qc[b, hq]
+                ids_read += int((offs[np.arange(wl.L), c + 1] - offs[np.arange(wl.L), c]).sum())
+        alg = (alg - Bn * Hkv * (n - nT) * KL / 8 + ids_read * 4 + Bn * Hq * wl.L * 8
+               + 2 * Bn * Hq * ((n + 31) // 32) * 4)
+
     def kern(r):
-        B_.decode_encoded(cfg, tq, mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n, ws,
-                          out=out)
+        if buckets:
+            B_.decode_buckets_encoded(cfg, tq, mps[r].buf.tables, mps[r].buf.center, mps[r].buf.key_norm, ks[r],
+                                      vs[r], 0, n, ws, out=out)
+        else:
+            B_.decode_encoded(cfg, tq, mps[r].buf.codes, mps[r].buf.center, mps[r].buf.key_norm, ks[r], vs[r], 0, n,
+                              ws, out=out)
 
     for r in range(R):
         kern(r)
@@ -235,6 +260,8 @@ def sweep_point(wl, dev, tW, peak, graph_launches=64):
     res = {"n": n, "B": Bn, "Hq": Hq, "Hkv": Hkv, "K": wl.K, "L": wl.L, "kernel_us": us, "tokens_per_s": Bn / us * 1e6,
            "alg_MB": alg / 1e6, "GBs": gbs, "frac": gbs / peak, "sampled_fraction": float(scount.float().mean()) /
            max(n - nT, 1), "replicas": R}
+    if buckets:
+        res.update(buckets=True, ids_read=ids_read, kernels="bucket_mark + decode5 (bitmap mode)")
     del mps, ks, vs, tk, tv
     torch.cuda.empty_cache()
     return res
@@ -415,15 +442,17 @@ def run_ours(args):
         sweep = []
         for spec in args.sweep.split(","):
             name, _, nn = spec.partition(":")
+            bk = name.endswith("b")  # "C2b:16384": the bucketed hash-table path
+            name = name[:-1] if bk else name
             wl_s = dataclasses.replace(synth.CONFIGS[name], n=int(nn)) if nn else synth.CONFIGS[name]
-            if wl_s == wl:
+            if wl_s == wl and not bk:
                 sweep.append({"n": n, "B": Bn, "Hq": Hq, "Hkv": Hkv, "K": wl.K, "L": wl.L, "kernel_us": kern_ms * 1e3,
                               "tokens_per_s": Bn / kern_ms * 1e3, "alg_MB": alg_bytes / 1e6, "GBs": achieved,
                               "frac": achieved / peak, "sampled_fraction": sampled_frac, "replicas": R})
                 continue
             tWs = tW if (wl_s.K, wl_s.L, wl_s.mips) == (wl.K, wl.L, wl.mips) else \
                 torch.from_numpy(synth.make_projections(wl_s.K, wl_s.L, wl_s.mips)).to(dev)
-            pt = sweep_point(wl_s, dev, tWs, peak)
+            pt = sweep_point(wl_s, dev, tWs, peak, buckets=bk)
             pt["config"] = name
             sweep.append(pt)
 
@@ -502,7 +531,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-steps-cap", type=int, default=200)
-    ap.add_argument("--sweep", default="C2:4096,C2:16384,C2:65536,C2:131072",
+    ap.add_argument("--sweep", default="C2:4096,C2:16384,C2:65536,C2:131072,C2b:16384,C2b:131072",
                     help="decode-kernel roofline vs context length: comma list of CONFIG[:n] ('' = off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

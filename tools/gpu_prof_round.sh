@@ -7,7 +7,7 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 300 > $OUT/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> $OUT/pytest_gpu.log
-timeout 900 python bench.py --sweep "C2:4096,C2:16384,C2:65536,C2:131072,C3" > $OUT/bench.log 2>&1
+timeout 900 python bench.py --sweep "C2:4096,C2:16384,C2:65536,C2:131072,C3,C2b:16384,C2b:131072,C3b" > $OUT/bench.log 2>&1
 echo "bench exit $?" >> $OUT/bench.log
 NCU=/usr/local/cuda/bin/ncu
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \

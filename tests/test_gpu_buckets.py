@@ -143,3 +143,79 @@ def test_bucket_limits():
     mp = pkg.MagicPIG(W, K=16, L=9, buckets=True)
     with pytest.raises(pkg.MagicPIGError):
         mp.build(torch.zeros((1, 1, 1000, 128), dtype=torch.bfloat16, device=_dev()))
+
+
+def test_bucketed_sequence_sharding_emulated():
+    """Sequence shards on one GPU with bucketed tables per shard: the union of the shards' S equals the
+    unsharded S, and the fixed-order merge of the shard partials equals the unsharded estimate (P12)."""
+    pkg = _pkg()
+    Bd = pkg.binding
+    wl = synth.Workload("bshard", 1850, B=1, Hq=4, Hkv=2, n=5000, K=10, L=150)
+    k, v, q = synth.make_batch(wl)
+    W = synth.make_projections(wl.K, wl.L, 1)
+    tW = torch.from_numpy(W).to(_dev())
+    tk_full, tv_full, tq = _bf(k), _bf(v), _bf(q)
+    full = pkg.MagicPIG(tW, K=wl.K, L=wl.L, buckets=True).build(tk_full)
+    sm_full = torch.zeros((1, 4, (wl.n + 31) // 32), dtype=torch.int32, device=_dev())
+    out_full = full.decode(tq, tk_full, tv_full, s_mask=sm_full)
+    cfg = full.cfg
+    dev = _dev()
+    cuts = [0, 1024 + 300, 2900, 5000]
+    P = len(cuts) - 1
+    ks_all = torch.zeros((P, 1, 2, 128, 2), dtype=torch.int64, device=dev)
+    cnt_all = torch.zeros((P, 1, 2), dtype=torch.int64, device=dev)
+    shards = []
+    for p in range(P):
+        a, b = cuts[p], cuts[p + 1]
+        tk = _bf(k[:, :, a:b])
+        ws = Bd.new_workspace(Bd.build_workspace_bytes(cfg, 1, 2, b - a), dev)
+        Bd.key_stats(cfg, tk, a, wl.n, ks_all[p], cnt_all[p], ws)
+        shards.append((a, b, tk, _bf(v[:, :, a:b]), ws))
+    key_sum = torch.zeros((1, 2, 128, 2), dtype=torch.int64, device=dev)
+    count = torch.zeros((1, 2), dtype=torch.int64, device=dev)
+    Bd.reduce_stats(0, ks_all, cnt_all, P, 1, 2, key_sum, count)
+    center = torch.zeros((1, 2, 128), dtype=torch.float32, device=dev)
+    r2_all = torch.zeros((P, 1, 2, 2), dtype=torch.int64, device=dev)
+    for p, (a, b, tk, tv, ws) in enumerate(shards):
+        Bd.key_norms(cfg, tk, a, wl.n, key_sum, count, center, r2_all[p], ws)
+    r2 = torch.zeros((1, 2, 2), dtype=torch.int64, device=dev)
+    Bd.reduce_stats(1, r2_all, None, P, 1, 2, r2, None)
+    parts = torch.zeros((P, 4, 130), dtype=torch.float32, device=dev)
+    masks = []
+    for p, (a, b, tk, tv, ws) in enumerate(shards):
+        codes = torch.zeros((Bd.codes_words(cfg, 1, 2, b - a),), dtype=torch.int32, device=dev)
+        knorm = torch.zeros((1, 2, b - a), dtype=torch.float32, device=dev)
+        Bd.build_tables(cfg, tk, a, wl.n, tW, center, r2, codes, knorm, ws)
+        tables = torch.zeros((Bd.bucket_tables_words(cfg, 1, 2, b - a),), dtype=torch.int32, device=dev)
+        Bd.build_buckets(cfg, codes, 1, 2, b - a, tables)
+        wsd = Bd.new_workspace(Bd.decode_workspace_bytes(cfg, 1, 4, 2, b - a), dev)
+        sm = torch.zeros((1, 4, (b - a + 31) // 32), dtype=torch.int32, device=dev)
+        Bd.decode_buckets(cfg, tq, tables, center, knorm, tk, tv, a, wl.n, tW, wsd, partial=parts[p], s_mask=sm)
+        masks.append((a, b, sm))
+    out = torch.zeros((1, 4, 128), dtype=torch.float32, device=dev)
+    Bd.merge_partials(parts, out)
+    torch.cuda.synchronize()
+    full_mask = sm_full.cpu().numpy().view(np.uint32)
+    for a, b, sm in masks:
+        mk = sm.cpu().numpy().view(np.uint32)
+        for row in range(4):
+            got = np.unpackbits(mk[0, row].view(np.uint8), bitorder="little")[: b - a]
+            want = np.unpackbits(full_mask[0, row].view(np.uint8), bitorder="little")[a:b]
+            np.testing.assert_array_equal(got, want)
+    for row in range(4):
+        assert _rel_err(out.cpu().numpy()[0, row], out_full.cpu().numpy()[0, row]) <= 2e-4
+
+
+def test_bucketed_session_matches_decode():
+    pkg = _pkg()
+    wl = synth.Workload("bsess", 1860, B=1, Hq=8, Hkv=2, n=3000, K=10, L=150)
+    k, v, q = synth.make_batch(wl)
+    W = synth.make_projections(wl.K, wl.L, wl.mips)
+    mp, tk = _build(wl, k, W)
+    tv, tq = _bf(v), _bf(q)
+    ref = mp.decode(tq, tk, tv).cpu()
+    sess = pkg.session(mp, tk, tv, wl.Hq)
+    sess.q_host.copy_(tq.cpu())
+    got = sess.step()
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)

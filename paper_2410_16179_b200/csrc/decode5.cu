@@ -539,13 +539,21 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                 *reinterpret_cast<float4*>(rec + gtid * PREC) = make_float4(f.mrun[gtid], f.srun[gtid], f.cnt[gtid], 0.0f);
             }
         }
-        __threadfence();
+        // arrival: the named barrier orders the group's record stores before thread 0's acq_rel atomic
+        // (release is cumulative), whose acquire half orders the merging CTA's loads after the other
+        // CTAs' releases -- no full memory fences (dbg bit 4: the old __threadfence pattern, for A/B)
+        if (a.dbg & 16) __threadfence();
         bar_named(2, NGW * 32);
-        if (gtid == 0) f.flag = atomicAdd(a.unit_ctr + u, 1u) == (uint32_t)(np - 1);
+        if (gtid == 0) {
+            uint32_t old;
+            if (a.dbg & 16) old = atomicAdd(a.unit_ctr + u, 1u);
+            else asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.unit_ctr + u) : "memory");
+            f.flag = old == (uint32_t)(np - 1);
+        }
         bar_named(2, NGW * 32);
         if (gtid == 0) V5_STAMP(22);
         if (!f.flag) return;
-        __threadfence();
+        if (a.dbg & 16) __threadfence();
         V5_STAMP(4);
         // warp per head, lane = 4 dims: the unit's records in fixed order, MB per round, all loads of a
         // round in flight together (record headers one per lane, broadcast by shuffles); running

@@ -82,10 +82,15 @@ def lib(load_only: bool = True):
     global _lib
     if _lib is None:
         path = _build.LIB
-        if not os.path.exists(path) or not load_only:
+        alt = os.environ.get("MAGICPIG_LIB")  # debug: A/B against another build of the library
+        if alt:
+            path = alt
+        elif not os.path.exists(path) or not load_only:
             path = _build.build()
         L = C.CDLL(path)
         for name, (args, res) in _SIGS.items():
+            if alt and not hasattr(L, name):
+                continue
             f = getattr(L, name)
             f.argtypes = args
             f.restype = res

@@ -25,6 +25,11 @@
 //                   (m, s, |S|, a) and the last CTA of a unit merges its partials
 //                   in fixed order (log-sum-exp, "recursive attention" P:171).
 //
+// Bucket mode (a.sbits != NULL, buckets.cu): S_g arrives as per-head bitmaps from the
+// bucketed hash-table query; the scan warps skip the code stream and only compact.
+// The unit merge keeps the records in registers (warp per head, lane = 4 dims, up to
+// 24 records per load round) and the arrival is one acq_rel atomic (no full fences).
+//
 // Tiles of a unit: nstatic static pieces, then nchunks code chunks.  CTA i owns
 // tiles [i*T/P, (i+1)*T/P), so the CTAs touching unit u are contiguous and the
 // partial of (u, i) lives at record u + i: the records of a unit are contiguous.
@@ -48,8 +53,6 @@ constexpr int XS = 272;                         // bf16 xbar tile row stride (by
 constexpr int QBS = 272;                        // bf16 query tile row stride (bytes)
 constexpr int PREC = PREC5;                     // record per head: m, s, |S_g|, 0, a[128]
 constexpr float INV_SQRT_D = 0.08838834764831845f;
-constexpr int PF_CHUNKS = 2;                    // code chunks prefetched into L2 ahead of the scan
-constexpr size_t PF_PIECE = 16384;              // bytes per bulk prefetch (one per lane)
 constexpr int MB = 24;                          // unit merge: records loaded per round (<= 32)
 
 // per-warp ring depth (table groups in flight per scan warp): ~104 KB of codes per CTA
@@ -70,6 +73,7 @@ struct __align__(16) Fixed {
     __align__(16) uint8_t qb16[8 * QBS];  // query rows of the gather's current unit (bf16, heads >= G zero)
     float c[HD];
     float qn[8], mrun[8], srun[8], scale[8], cnt[8];
+    float Mm[8], Sm[8], Cm[8], fo[8];  // unit merge: running max, sum, |S|, block rescale
     float zl[RB][8], zd[RB][8], w[RB][8];
     uint32_t s_sel[8][32];
     uint32_t s_tm[32];
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
     Fixed& f = *reinterpret_cast<Fixed*>(dsm + a.v5_off_fixed);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t T = a.v5_tiles, P = gridDim.x, tpu = a.nstatic + a.nchunks * a.v5_hs;
+    const int64_t T = a.v5_tiles, P = gridDim.x, tpu = a.nstatic + a.nchunks;
     const int64_t t0 = (int64_t)blockIdx.x * T / P, t1 = ((int64_t)blockIdx.x + 1) * T / P;
     const long long t_start = clock64();
     if (a.timeline && tid == 0) a.timeline[(size_t)blockIdx.x * 32] = gtimer();
@@ -225,73 +229,46 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
         // ===================== scan warps
         constexpr int D = ring_depth(QG);
         uint8_t* myring = ring + (size_t)warp * D * GB;
-        // A chunk tile is a whole 1024-key chunk (hs = 1) or one half of it (hs = 2: 512 keys, for
-        // small problems, so that the gather of a half overlaps the scan of the next).  With hs = 2 a
-        // warp step covers two table groups: lanes 0-15 the 16 key blocks of the half for group j,
-        // lanes 16-31 the same blocks for group j+1 (256-B contiguous pieces per column quad).
-        // This CTA's chunk tiles are consecutive global chunk tiles [gct0, gct1) (chunk tiles of a
-        // unit follow its static pieces, chunks of consecutive units are adjacent in memory).
-        const int hs = a.v5_hs, hsl = hs == 2 ? 1 : 0, LPG = 32 >> hsl;
-        const int lane_grp = lane >> (5 - hsl), blk = lane & (LPG - 1);
-        const int64_t ctpu = a.nchunks * hs;  // chunk tiles per unit
-        auto ctiles_before = [&](int64_t t) { return (t / tpu) * ctpu + max(t % tpu - a.nstatic, (int64_t)0); };
-        const int64_t gct1 = ctiles_before(t1);
+        // this CTA's chunk tiles are the consecutive global chunks [gc0, gc1) (chunk tiles of a unit
+        // follow its static pieces, chunks of consecutive units are adjacent in memory)
+        auto chunks_before = [&](int64_t t) { return (t / tpu) * a.nchunks + max(t % tpu - a.nstatic, (int64_t)0); };
+        const int64_t gc1 = chunks_before(t1);
         const size_t CB = (size_t)a.KLq * 512;  // code bytes per chunk
         const uint8_t* codes_b = reinterpret_cast<const uint8_t*>(a.codes);
-        const size_t lane_off = (size_t)lane_grp * GB + (size_t)blk * 16;
-        // issue iterator over this warp's (chunk tile, group) sequence; ring write/read pointers rotate
-        int64_t it_c = ctiles_before(t0);
-        int it_j = warp * hs;
-        const bool has_groups = warp * hs < a.ngroups;
+        // issue iterator over this warp's (chunk, group) sequence: a source pointer that steps by
+        // NSW groups and jumps to the next chunk; ring write/read pointers rotate (no divisions)
+        int64_t it_c = chunks_before(t0);
+        int it_j = warp;
+        const bool has_groups = warp < a.ngroups;
+        const uint8_t* it_src = codes_b + (size_t)it_c * CB + (size_t)warp * GB + lane * 16;
         uint8_t* const ring_end = myring + (size_t)D * GB;
         uint8_t* wr = myring + lane * 16;
         const uint8_t* rd = myring + lane * 16;
         auto issue = [&]() {
-            if (has_groups && it_c < gct1) {
-                if (it_j + lane_grp < a.ngroups) {
-                    const uint8_t* src = codes_b + (size_t)(it_c >> hsl) * CB + (size_t)(it_c & hsl) * (LPG * 16) +
-                                         (size_t)it_j * GB + lane_off;
+            if (has_groups && it_c < gc1) {
 #pragma unroll
-                    for (int q = 0; q < QG; q++) cp_async16(wr + q * 512, src + q * 512);
-                }
-                it_j += NSW * hs;
+                for (int q = 0; q < QG; q++) cp_async16(wr + q * 512, it_src + q * 512);
+                it_j += NSW;
                 if (it_j >= a.ngroups) {
-                    it_j = warp * hs;
+                    it_j = warp;
                     it_c++;
+                    it_src = codes_b + (size_t)it_c * CB + (size_t)warp * GB + lane * 16;
+                } else {
+                    it_src += NSW * GB;
                 }
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
             wr += GB;
             if (wr >= ring_end) wr -= (size_t)D * GB;
         };
-        // L2 prefetch of the first PF_CHUNKS chunks of this CTA's code range: HBM streams at full rate
-        // while the query codes are being encoded (the ring alone holds ~half a chunk); further chunks
-        // are prefetched PF_CHUNKS ahead as the scan reaches them (bulk prefetch: no SM issue cost)
-        const int64_t gc0 = ctiles_before(t0) >> hsl, gc1 = (gct1 + hs - 1) >> hsl;  // chunks
-        auto prefetch_chunk = [&](int64_t c) {
-            if (c < gc1 && (size_t)lane * PF_PIECE < CB) {
-                const size_t off = (size_t)lane * PF_PIECE;
-                const uint32_t len = (uint32_t)min((size_t)PF_PIECE, CB - off);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes_b + (size_t)c * CB + off), "r"(len)
-                             : "memory");
-            }
-        };
         // bucket mode (a.sbits != NULL): S comes from the bucketed hash-table query (buckets.cu) as
         // per-head bitmaps; the scan warps only read them and compact (no code stream)
         const bool dense = a.sbits == nullptr;
-        if (warp == 0 && !(a.dbg & 1) && dense)
-            for (int64_t c = gc0; c < gc0 + PF_CHUNKS; c++) prefetch_chunk(c);
-        // the ring is filled only after the query masks are built (from L2, where the prefetch put
-        // the codes): a ring fill issued first queues ~100 KB of loads ahead of the query-code load
-        // and delays the whole scan (dbg bit 2: old order, for A/B)
-        bool primed = false;
-        if (a.dbg & 4) {
+        if (dense) {
 #pragma unroll 1
             for (int k = 0; k < D; k++) issue();
-            primed = true;
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
-        if (tid == 0) V5_STAMP(7);
         const StaticRanges sr = static_ranges(a);
         const int ncolsP = a.ngroups * TG * K;
         int64_t cur_u = -1;
@@ -303,37 +280,25 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
             const int64_t b = u / a.Hkv, hkv = u % a.Hkv;
             const int64_t qh0 = b * a.Hq + hkv * G;
             if (!is_static) {
-                const int64_t ct = r - a.nstatic, chunk = ct >> hsl;
-                const int64_t cbase = chunk * KCHUNK + (ct & hsl) * (LPG * 32);  // first key of the tile
-                if (warp == 0 && (a.dbg & 2) && (ct & hsl) == 0 && dense) {
-                    const int64_t gc = u * a.nchunks + chunk + PF_CHUNKS;
-                    if (gc >= gc0 + PF_CHUNKS) prefetch_chunk(gc);
-                }
+                const int64_t chunk = r - a.nstatic;
+                const int64_t cbase = chunk * KCHUNK;
                 if (dense) {
                 if (u != cur_u) {  // query masks of unit u: QX[c][g] = qbit ? 0 : ~0 (P ^ QX = 1 where bits agree)
                     bar_named(1, NSW * 32);
                     for (int e = tid; e < G * a.KLw; e += NSW * 32) qbw[e] = __ldcg(a.qbits + qh0 * a.KLw + e);
                     bar_named(1, NSW * 32);
-                    if (tid == 0 && t == t0) V5_STAMP(8);
-                    for (int c = tid; c < ncolsP; c += NSW * 32) {  // thread per column, G masks
-                        const bool live = c < a.KL;
-#pragma unroll
-                        for (int g = 0; g < G; g++)
-                            qx[c * G + g] = (live && ((qbw[g * a.KLw + (c >> 5)] >> (c & 31)) & 1u)) ? 0u : 0xffffffffu;
+                    for (int e = tid; e < ncolsP * G; e += NSW * 32) {
+                        const int c = e / G, g = e % G;
+                        qx[e] = (c < a.KL && ((qbw[g * a.KLw + (c >> 5)] >> (c & 31)) & 1u)) ? 0u : 0xffffffffu;
                     }
                     bar_named(1, NSW * 32);
                     cur_u = u;
                     if (tid == 0 && t == t0) V5_STAMP(1);
                 }
-                if (!primed) {
-#pragma unroll 1
-                    for (int k = 0; k < D; k++) issue();
-                    primed = true;
-                }
                 uint32_t s1[G], s2[G];
 #pragma unroll
                 for (int g = 0; g < G; g++) s1[g] = s2[g] = 0u;
-                for (int j = warp * hs; j < a.ngroups; j += NSW * hs) {
+                for (int j = warp; j < a.ngroups; j += NSW) {
                     asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
                     __syncwarp();
                     uint4 Pw[QG];
@@ -344,12 +309,10 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                     __syncwarp();
                     issue();  // refill the slot just read
                     const uint32_t* wv = reinterpret_cast<const uint32_t*>(Pw);
-                    const int jj = j + lane_grp;
-                    const bool live = jj < a.ngroups;
-                    const uint32_t* qrow = qx + (size_t)(live ? jj : j) * TG * K * G;
+                    const uint32_t* qrow = qx + (size_t)j * TG * K * G;
 #pragma unroll
                     for (int tt = 0; tt < TG; tt++) {
-                        if (live && (TG == 1 || tt == 0 || jj * TG + tt < a.L)) {
+                        if (TG == 1 || tt == 0 || j * TG + tt < a.L) {
                             uint32_t m[G];
 #pragma unroll
                             for (int g = 0; g < G; g++) m[g] = 0xffffffffu;
@@ -380,15 +343,6 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                     }
                 }
                 if (t == t0 && lane == 0) V5_STAMP(11 + warp);
-                if (hsl) {  // lanes l and l + 16 hold the same key block for different table groups
-#pragma unroll
-                    for (int g = 0; g < G; g++) {
-                        const uint32_t o1 = __shfl_down_sync(0xffffffffu, s1[g], 16);
-                        const uint32_t o2 = __shfl_down_sync(0xffffffffu, s2[g], 16);
-                        s2[g] |= o2 | (s1[g] & o1);
-                        s1[g] |= o1;
-                    }
-                }
 #pragma unroll
                 for (int g = 0; g < G; g++) {
                     s_part[((warp * G + g) * 2 + 0) * 32 + lane] = s1[g];
@@ -402,11 +356,9 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                                    range_mask(base, 0, a.n_local);
                 }
                 bar_named(1, NSW * 32);
-                if (tid == 0 && t == t0) V5_STAMP(9);
                 // warps -> CTA: (a1,a2)+(b1,b2) = (a1|b1, a2|b2|(a1&b1)); S_g = count >= minc on D
                 if (tid < G * 32) {
                     const int g = tid >> 5;
-                    const int64_t nwb = (a.n_local + 31) >> 5;
                     uint32_t sel;
                     if (dense) {
                         uint32_t f1 = 0, f2 = 0;
@@ -419,12 +371,11 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                         }
                         sel = a.minc == 1 ? f1 : f2;
                     } else {
-                        const int64_t wi = (cbase >> 5) + lane;
-                        sel = (lane < LPG && wi < nwb) ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
+                        const int64_t nwb = (a.n_local + 31) >> 5, wi = chunk * 32 + lane;
+                        sel = wi < nwb ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
                     }
                     const int64_t base = cbase + lane * 32;
                     uint32_t v = sel & range_mask(base, 0, a.n_local) & ~f.s_tm[lane];
-                    if (lane >= LPG) v = 0u;
                     f.s_sel[g][lane] = v;
                     int cnt = __popc(v);
 #pragma unroll
@@ -432,12 +383,11 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                     if (lane == 0) f.s_cnt[g] = cnt;
                     if (a.s_mask) {
                         const int64_t nw = (a.n_local + 31) >> 5;
-                        const int64_t widx = (cbase >> 5) + lane;
-                        if (lane < LPG && widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
+                        const int64_t widx = chunk * 32 + lane;
+                        if (widx < nw) a.s_mask[(qh0 + g) * nw + widx] = v;
                     }
                 }
                 bar_named(1, NSW * 32);
-                if (tid == 0 && t == t0) V5_STAMP(10);
                 if (warp == 0) {  // exclusive scan of the 32 block counts of union_g S_g
                     uint32_t uu = 0;
 #pragma unroll
@@ -472,9 +422,8 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                     for (int g = 0; g < 8; g++) D.cnt[g] = 0;
                 }
             } else {
-                const int64_t ct = r - a.nstatic;
-                const int64_t cbase = (ct >> hsl) * KCHUNK + (ct & hsl) * (LPG * 32);
-                for (int bl = warp; bl < LPG; bl += NSW) {
+                const int64_t cbase = (r - a.nstatic) * KCHUNK;
+                for (int bl = warp; bl < 32; bl += NSW) {
                     uint32_t uu = 0, sg[G];
 #pragma unroll
                     for (int g = 0; g < G; g++) {
@@ -541,19 +490,16 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
         }
         // arrival: the named barrier orders the group's record stores before thread 0's acq_rel atomic
         // (release is cumulative), whose acquire half orders the merging CTA's loads after the other
-        // CTAs' releases -- no full memory fences (dbg bit 4: the old __threadfence pattern, for A/B)
-        if (a.dbg & 16) __threadfence();
+        // CTAs' releases -- no full memory fences
         bar_named(2, NGW * 32);
         if (gtid == 0) {
             uint32_t old;
-            if (a.dbg & 16) old = atomicAdd(a.unit_ctr + u, 1u);
-            else asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.unit_ctr + u) : "memory");
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.unit_ctr + u) : "memory");
             f.flag = old == (uint32_t)(np - 1);
         }
         bar_named(2, NGW * 32);
         if (gtid == 0) V5_STAMP(22);
         if (!f.flag) return;
-        if (a.dbg & 16) __threadfence();
         V5_STAMP(4);
         // warp per head, lane = 4 dims: the unit's records in fixed order, MB per round, all loads of a
         // round in flight together (record headers one per lane, broadcast by shuffles); running
@@ -613,6 +559,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
             }
         }
         if (gtid == 0) a.unit_ctr[u] = 0u;
+        bar_named(2, NGW * 32);  // merge buffer (row stages) free again
         V5_STAMP(5);
     };
 
@@ -665,39 +612,13 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
     int di = 0;
     bool first_batch = true;
     long long acc_df = 0, acc_rw = 0;
-    // row staging runs ahead of the compute over a flat (descriptor, batch) sequence: batches are staged
-    // up to NSTAGE - 1 ahead of the one being computed.  In bucket mode (descriptors arrive faster than
-    // they are gathered) the cursor also crosses into the next descriptor, so its first rows are in
-    // flight while the current one finishes; in dense mode it stops at the descriptor boundary.
-    const bool cross = a.sbits != nullptr;
-    const int ndesc = (int)(t1 - t0);
-    int sdi = 0, sbt = 0;  // next (descriptor, batch) to stage
-    uint32_t cseq = 0;     // batches computed so far (= stage buffer sequence)
-    auto stage_upto = [&](uint32_t limit) {
-        // at most one descriptor ahead: descriptor di + 2 reuses the slot of di, which is released only
-        // after di is computed (waiting for it here would deadlock)
-        while (rseq < limit && sdi < ndesc && sdi <= di + (cross ? 1 : 0)) {
-            if (sdi > di) mbar_wait(&f.dfull[sdi & 1], (uint32_t)((sdi >> 1) & 1));
-            const Desc& Ds = f.desc[sdi & 1];
-            const int nbs = (Ds.n + RB - 1) / RB;
-            if (sbt < nbs) {
-                stage(Ds, sbt * RB, min(RB, Ds.n - sbt * RB), Ds.unit);
-                sbt++;
-            }
-            if (sbt >= nbs) {
-                sdi++;
-                sbt = 0;
-            }
-        }
-    };
     if (t0 < t1) {  // the first unit's data while the scan warps work
         cur_u = t0 / tpu;
         load_unit(cur_u);
     }
     for (int64_t t = t0; t < t1; t++, di++) {
         long long tg0 = clock64();
-        if (a.dbg & 8) mbar_wait_sleep(&f.dfull[di & 1], (uint32_t)((di >> 1) & 1));
-        else mbar_wait(&f.dfull[di & 1], (uint32_t)((di >> 1) & 1));
+        mbar_wait_sleep(&f.dfull[di & 1], (uint32_t)((di >> 1) & 1));
         acc_df += clock64() - tg0;
         const Desc& D = f.desc[di & 1];
         const int64_t u = D.unit;
@@ -711,16 +632,15 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
         if (gtid < G) f.cnt[gtid] += (float)D.cnt[gtid];
         const int n = D.n;
         const int nbatch = (n + RB - 1) / RB;
-        if (nbatch == 0 && sdi == di) sdi++, sbt = 0;  // nothing to stage for an empty descriptor
+        const uint32_t rbase = rseq;
+        for (int bt = 0; bt < 2 && bt < nbatch; bt++) stage(D, bt * RB, min(RB, n - bt * RB), u);
         for (int bt = 0; bt < nbatch; bt++) {
-            stage_upto(cseq + NSTAGE);
-            const uint32_t k = cseq++;
+            if (bt + 2 < nbatch) stage(D, (bt + 2) * RB, min(RB, n - (bt + 2) * RB), u);
+            const uint32_t k = rbase + bt;
             const uint8_t* buf = rows + (size_t)(k % NSTAGE) * RB * ROWB;
             long long tr0 = clock64();
-            if (a.dbg & 8) mbar_wait_sleep(&f.rowbar[k % NSTAGE], (k / NSTAGE) & 1);
-            else mbar_wait(&f.rowbar[k % NSTAGE], (k / NSTAGE) & 1);
+            mbar_wait_sleep(&f.rowbar[k % NSTAGE], (k / NSTAGE) & 1);
             acc_rw += clock64() - tr0;
-            if (first_batch && gtid == 0) V5_STAMP(29);
             const int nb = min(RB, n - bt * RB);
             // (a) xbar = bf16(fl32(k - c)) of the batch rows (cvt.rn.bf16x2.f32)
 #pragma unroll
@@ -743,7 +663,6 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                 *reinterpret_cast<uint4*>(xt + rr * XS + dg * 16) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
             }
             bar_named(2, NGW * 32);
-            if (first_batch && gtid == 0) V5_STAMP(30);
             // (b) tensor cores: warp (mt, which) = 16 rows x {raw keys -> logits, xbar -> hashed dots}
             {
                 const int mt = gw & 1, which = gw >> 1;
@@ -806,7 +725,6 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                 }
             }
             bar_named(2, NGW * 32);
-            if (first_batch && gtid == 0) V5_STAMP(31);
             // (d) a[g][d] = a * scale + sum_rows w * v on tensor cores (tf32 m16n8k8, fp32 accumulate):
             // A = weights [heads x rows], B = V [rows x dims]; warp gw owns dims 32 gw .. 32 gw + 31
             {
@@ -855,12 +773,10 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
 // ---- host: shared-memory layout and launch
 static size_t al128(size_t x) { return (x + 127) & ~(size_t)127; }
 
-// chunk tiles per chunk: 1 (whole 1024-key chunks).  512-key halves (dbg bit 6) let a CTA pipeline the
-// gather of one half with the scan of the next, but measured slower at C2 on B200 (21.9 vs 19.5 us:
-// the per-tile combine/compaction cost does not halve with the tile), so they are a tested option only
+// chunk tiles per 1024-key chunk: 1 (512-key half tiles were measured slower and removed)
 int decode5_halves(const DecodeArgs& a, int nsm) {
+    (void)a;
     (void)nsm;
-    if (a.dbg & 64) return 2;
     return 1;
 }
 
@@ -901,8 +817,8 @@ static int launch5_kg(DecodeArgs a, int nsm, int max_smem, cudaStream_t st) {
     auto kern = v5::decode5_kernel<K, G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return MAGICPIG_ECUDA;
-    a.v5_hs = decode5_halves(a, nsm);
-    a.v5_tiles = a.B * a.Hkv * (a.nstatic + a.nchunks * a.v5_hs);
+    a.v5_hs = 1;
+    a.v5_tiles = a.B * a.Hkv * (a.nstatic + a.nchunks);
     const int64_t P = a.v5_tiles < nsm ? a.v5_tiles : nsm;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)P);

@@ -1,0 +1,16 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+OUT=gpurun_out/${TAG:-libab}
+mkdir -p $OUT
+timeout 500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_buckets.py -m gpu -q -x -p no:cacheprovider --timeout 200 > $OUT/pytest.log 2>&1
+echo "pytest exit $?" >> $OUT/pytest.log
+for v in base cur5 base cur5; do
+  case $v in
+    base) L=$PWD/ablib/libmagicpig_base.so;;
+    cur5) L="";;
+  esac
+  echo "== $v" >> $OUT/dec.log
+  MAGICPIG_LIB=$L timeout 200 python tools/dec_bench.py C3 reps=2 >> $OUT/dec.log 2>&1
+  MAGICPIG_LIB=$L timeout 100 python tools/dec_bench.py C2 >> $OUT/dec.log 2>&1
+done

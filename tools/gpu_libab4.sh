@@ -1,0 +1,19 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+OUT=gpurun_out/${TAG:-libab}
+mkdir -p $OUT
+for v in base va vb cur va vb; do
+  case $v in
+    cur) L="";;
+    *) L=$PWD/ablib/libmagicpig_$v.so;;
+  esac
+  echo "== $v" >> $OUT/dec.log
+  MAGICPIG_LIB=$L timeout 200 python tools/dec_bench.py C3 reps=2 >> $OUT/dec.log 2>&1
+  MAGICPIG_LIB=$L timeout 100 python tools/dec_bench.py C2 >> $OUT/dec.log 2>&1
+  [ $v != base ] && MAGICPIG_LIB=$L timeout 200 python tools/dec_bench.py C3 reps=2 buckets=1 >> $OUT/dec.log 2>&1
+done
+for v in va vb; do
+  MAGICPIG_LIB=$PWD/ablib/libmagicpig_$v.so timeout 300 python -m pytest tests/test_gpu_buckets.py tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider --timeout 200 -k "not k4" > $OUT/pytest_$v.log 2>&1
+  echo "pytest exit $?" >> $OUT/pytest_$v.log
+done

@@ -441,10 +441,14 @@ def run_ours(args):
         import dataclasses
         sweep = []
         for spec in args.sweep.split(","):
-            name, _, nn = spec.partition(":")
+            name, _, rest = spec.partition(":")
+            nn, _, ov = rest.partition(":")  # "C2:16384:mips=0+min_collisions=1": variant flags (NEXT-4)
             bk = name.endswith("b")  # "C2b:16384": the bucketed hash-table path
             name = name[:-1] if bk else name
             wl_s = dataclasses.replace(synth.CONFIGS[name], n=int(nn)) if nn else synth.CONFIGS[name]
+            over = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in ov.split("+") if kv}
+            if over:
+                wl_s = dataclasses.replace(wl_s, **over)
             if wl_s == wl and not bk:
                 sweep.append({"n": n, "B": Bn, "Hq": Hq, "Hkv": Hkv, "K": wl.K, "L": wl.L, "kernel_us": kern_ms * 1e3,
                               "tokens_per_s": Bn / kern_ms * 1e3, "alg_MB": alg_bytes / 1e6, "GBs": achieved,
@@ -454,6 +458,8 @@ def run_ours(args):
                 torch.from_numpy(synth.make_projections(wl_s.K, wl_s.L, wl_s.mips)).to(dev)
             pt = sweep_point(wl_s, dev, tWs, peak, buckets=bk)
             pt["config"] = name
+            if over:
+                pt["variant"] = over
             sweep.append(pt)
 
     cpu = None

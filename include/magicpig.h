@@ -251,8 +251,25 @@ int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, const uint16_
                                        unsigned long long* timeline, int64_t timeline_len, void* ws,
                                        size_t ws_bytes, void* stream);
 
+/* Debug: one decode step (encode + Query + estimator) that also exports the sets
+ * the estimator actually used:
+ *   s_mask[B][Hq][ceil(n_local/32)]    S_g restricted to D (the Query result), or NULL
+ *   weighted[B][Hq][ceil(n_local/32)]  bit (g, i) set iff key i received a finite
+ *                                      weight for head g in the estimator's gather,
+ *                                      i.e. the compacted list it consumed: S_g u T
+ *                                      (zeroed by this call)
+ * codes (dense) or tables (bucketed, magicpig_build_buckets) selects the Query path.
+ * Requires decode kernel 6 (the default).                                       */
+int magicpig_debug_decode_sets(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
+                               const int32_t* tables, const float* center, const float* key_norm, const uint16_t* k,
+                               const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset,
+                               int64_t n_global, const float* W, float* out, uint32_t* s_mask, uint32_t* weighted,
+                               void* ws, size_t ws_bytes, void* stream);
+
 /* Selects the decode kernel for subsequent decode calls of this process (a debug
- * knob for A/B measurement; default 5): 5 = persistent warp-specialised kernel
+ * knob for A/B measurement; default 6): 6 = Query kernel (dense code scan, or the
+ * bucketed tables) writing per-head S bitmaps, then the estimator kernel (all warps
+ * gather 16-row slabs independently); 5 = persistent warp-specialised fused kernel
  * (one CTA per SM over a contiguous tile range; used whenever its shared-memory
  * layout fits, else 4), 4 = one thread-block cluster per 1024-key chunk.  Both
  * compute the same S bit for bit.  For kernel 5 the timeline slots are clock64

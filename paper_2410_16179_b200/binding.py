@@ -61,6 +61,8 @@ _SIGS = {
     "magicpig_decode_buckets_encoded": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p,
                                          _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_set_decode_kernel": ([_i], _i),
+    "magicpig_debug_decode_sets": ([_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p,
+                                    _p, _p, _sz, _p], _i),
     "magicpig_export_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
     "magicpig_import_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
     "magicpig_query_codes": ([_p, _p, _i64, _i64, _p, _p, _p, _sz, _p], _i),
@@ -291,8 +293,21 @@ def debug_decode_timeline(cfg, q, codes, center, key_norm, k, v, W, out, timelin
     return int(rc)
 
 
+def debug_decode_sets(cfg, q, codes, tables, center, key_norm, k, v, seq_offset, n_global, W, ws, out, s_mask,
+                      weighted):
+    """One decode step that also exports S_g (restricted to D) and the (head, key) pairs that received a
+    weight in the estimator's gather (S_g u T), as [B][Hq][ceil(n/32)] uint32 bitmaps."""
+    B, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    _check(lib().magicpig_debug_decode_sets(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(tables), _ptr(center),
+                                            _ptr(key_norm), _ptr(k), _ptr(v), B, Hkv, n, seq_offset, n_global, _ptr(W),
+                                            _ptr(out), _ptr(s_mask), _ptr(weighted), _ptr(ws), ws.numel(), _stream()),
+           "debug_decode_sets")
+
+
 def set_decode_kernel(version: int):
-    """Debug knob: 5 = persistent warp-specialised decode kernel (default), 4 = cluster-per-chunk."""
+    """Debug knob: 6 = Query kernel + estimator kernel (default), 5 = persistent fused kernel,
+    4 = cluster-per-chunk."""
     _check(lib().magicpig_debug_set_decode_kernel(int(version)), "set_decode_kernel")
 
 

@@ -118,13 +118,18 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_build_kernel(const uint32_t
     }
 }
 
-// grid (Hq, B); dynamic smem = 2 * nw words + 2 * (L + 1) ints.  qbits [B][Hq][KLw] (bit j = column j of q_g).
+// grid (Hq, B); dynamic smem = 2 * nw words + 2 * L + 1 ints.  qbits [B][Hq][KLw] (bit j = column j of q_g).
 // Latency structure: one round for every table's bucket range (thread per table), a block scan of the
-// bucket sizes, then all ids of all buckets flattened over the CTA (each thread's loads independent).
+// bucket sizes, then the ids of all L buckets as one flattened array split over the CTA in runs of BM_RUN
+// consecutive entries per thread (one binary search per run, then a forward walk over the tables), all
+// loads of a run in flight before the shared-memory atomics.  Bucket sizes are very skewed (the query's
+// bucket can hold thousands of keys), so the split is over entries, not over tables.
+constexpr int BM_RUN = 8;
 __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t* __restrict__ qbits,
                                                                   const int32_t* __restrict__ tables, int64_t Hq,
                                                                   int64_t Hkv, int64_t n_local, int K, int L, int KLw,
                                                                   int minc, uint32_t* __restrict__ sbits) {
+    asm volatile("griddepcontrol.launch_dependents;");  // the estimator kernel may start its prologue
     extern __shared__ uint32_t seen[];  // seen1[nw], seen2[nw], lo[L], start[L + 1]
     __shared__ int warp_tot[33];
     const int64_t hq = blockIdx.x, b = blockIdx.y;
@@ -156,25 +161,26 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
     if (tid == 0) start[L] = total;
     __syncthreads();
     const int32_t* ids0 = tu + (size_t)L * (nb + 1);
-    constexpr int ILP = 8;
-    for (int e0 = tid; e0 < total; e0 += blockDim.x * ILP) {
-        int ids[ILP];
+    for (int e0 = tid * BM_RUN; e0 < total; e0 += blockDim.x * BM_RUN) {
+        int lo = 0, hi = L;  // table of flat index e0: last t with start[t] <= e0
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (start[mid] <= e0) lo = mid;
+            else hi = mid;
+        }
+        int t = lo, tnext = start[t + 1];
+        int ids[BM_RUN];
 #pragma unroll
-        for (int j = 0; j < ILP; j++) {
-            const int e = e0 + j * blockDim.x;
+        for (int j = 0; j < BM_RUN; j++) {
+            const int e = e0 + j;
             ids[j] = -1;
             if (e < total) {
-                int lo = 0, hi = L;  // table of flat index e: last t with start[t] <= e
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (start[mid] <= e) lo = mid;
-                    else hi = mid;
-                }
-                ids[j] = __ldg(ids0 + (size_t)lo * n_local + lo_s[lo] + (e - start[lo]));
+                while (e >= tnext) tnext = start[++t + 1];
+                ids[j] = __ldg(ids0 + (size_t)t * n_local + lo_s[t] + (e - start[t]));
             }
         }
 #pragma unroll
-        for (int j = 0; j < ILP; j++) {
+        for (int j = 0; j < BM_RUN; j++) {
             if (ids[j] >= 0) {
                 const int i = ids[j];
                 const uint32_t bit = 1u << (i & 31);

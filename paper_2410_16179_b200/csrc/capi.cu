@@ -34,10 +34,11 @@ static int max_smem_optin() {
     return n;
 }
 
-// decode kernel selection (debug knob, magicpig_debug_set_decode_kernel): 5 = persistent
-// warp-specialised kernel (default; falls back to 4 when its shared memory does not fit),
-// 4 = one cluster per chunk
-static std::atomic<int> g_decode_kernel{5};
+// decode kernel selection (debug knob, magicpig_debug_set_decode_kernel): 6 = Query kernel (dense
+// scan6 or bucket_mark) -> S bitmaps -> estimator kernel (attend.cu) (default); 5 = persistent
+// warp-specialised fused kernel (falls back to 4 when its shared memory does not fit), 4 = one
+// cluster per chunk.  5 and 4 are kept as A/B arms; all compute the same S bit for bit.
+static std::atomic<int> g_decode_kernel{6};
 
 static bool cfg_ok(const magicpig_config* c) {
     if (!c) return false;
@@ -269,7 +270,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
                        int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
                        float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
                        void* stream, unsigned long long* timeline, int64_t timeline_len, int64_t* grid_out,
-                       const int32_t* tables = nullptr) {
+                       const int32_t* tables = nullptr, uint32_t* weighted = nullptr) {
     if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
     if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
     const int64_t G = Hq / Hkv;
@@ -346,6 +347,39 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
     const int kver = g_decode_kernel.load();
+    if (kver % 10 == 6 && !timeline) {
+        // Query(HT, q_code) -> S bitmaps: bucketed tables or the dense code scan (PDL after the encode)
+        int rc;
+        if (tables) {
+            rc = launch_bucket_mark(w.qbits, tables, B, Hq, Hkv, n_local, cfg->K, cfg->L, g.KLw,
+                                    cfg->min_collisions, w.sbits, st);
+        } else {
+            ScanArgs sa;
+            memset(&sa, 0, sizeof(sa));
+            sa.qbits = w.qbits;
+            sa.codes = codes;
+            sa.sbits = w.sbits;
+            sa.B = B, sa.Hkv = Hkv, sa.Hq = Hq, sa.n_local = n_local, sa.nchunks = g.nchunks;
+            sa.tiles = B * Hkv * g.nchunks;
+            sa.K = cfg->K, sa.L = cfg->L, sa.KL = g.KL, sa.KLw = g.KLw, sa.KLq = g.KLq, sa.ngroups = g.ngroups;
+            sa.minc = cfg->min_collisions;
+            rc = launch_scan6(sa, num_sms(), max_smem_optin(), st);
+        }
+        if (rc) return rc;
+        // estimator over S_g u T
+        AttendArgs aa;
+        memset(&aa, 0, sizeof(aa));
+        aa.q = q, aa.center = center, aa.key_norm = key_norm, aa.k = k, aa.v = v, aa.sbits = w.sbits;
+        aa.B = B, aa.Hkv = Hkv, aa.Hq = Hq, aa.n_local = n_local, aa.seq_offset = seq_offset;
+        aa.n_global = n_global, aa.nchunks = g.nchunks, aa.nstatic = a.nstatic;
+        aa.tiles = B * Hkv * (g.nchunks + a.nstatic);
+        aa.K = cfg->K, aa.L = cfg->L, aa.minc = cfg->min_collisions, aa.sink = cfg->sink, aa.local = cfg->local;
+        aa.out = out, aa.partial = partial, aa.s_count = s_count, aa.s_mask = s_mask, aa.weighted = weighted;
+        aa.unit_ctr = w.unit_ctr, aa.parts = w.parts, aa.status = w.status;
+        if (grid_out) *grid_out = aa.tiles < num_sms() ? aa.tiles : num_sms();
+        return launch_attend(aa, num_sms(), max_smem_optin(), st);
+    }
+    if (weighted) return MAGICPIG_EINVAL;  // the weighted-set export exists on the v6 path only
     bool v5 = kver % 10 == 5 || tables;  // bucket mode runs on the persistent kernel only
     a.dbg = kver / 10;
     if (v5) {
@@ -371,7 +405,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
 }
 
 extern "C" int magicpig_debug_set_decode_kernel(int version) {
-    if (version % 10 != 4 && version % 10 != 5) return MAGICPIG_EINVAL;
+    if (version % 10 != 4 && version % 10 != 5 && version % 10 != 6) return MAGICPIG_EINVAL;
     g_decode_kernel.store(version);
     return MAGICPIG_OK;
 }
@@ -447,6 +481,22 @@ int magicpig_decode_buckets_encoded(const magicpig_config* cfg, const uint16_t* 
     if (n_local > 0 && !tables) return MAGICPIG_EINVAL;
     return decode_impl(cfg, q, Hq, nullptr, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
                        partial, s_count, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables);
+}
+
+int magicpig_debug_decode_sets(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
+                               const int32_t* tables, const float* center, const float* key_norm, const uint16_t* k,
+                               const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset,
+                               int64_t n_global, const float* W, float* out, uint32_t* s_mask, uint32_t* weighted,
+                               void* ws, size_t ws_bytes, void* stream) {
+    if (!W || !weighted || (n_local > 0 && !codes && !tables) || n_local < 1) return MAGICPIG_EINVAL;
+    if (!cfg_ok(cfg) || Hq < Hkv || Hkv < 1 || B < 1 || Hq % Hkv) return MAGICPIG_EINVAL;
+    if (g_decode_kernel.load() % 10 != 6) return MAGICPIG_EINVAL;
+    if (cudaMemsetAsync(weighted, 0, (size_t)B * Hq * ((n_local + 31) / 32) * 4, S(stream)) != cudaSuccess)
+        return MAGICPIG_ECUDA;
+    int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
+    if (rc) return rc;
+    return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
+                       nullptr, nullptr, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, weighted);
 }
 
 int magicpig_merge_partials(const float* parts, int P, int64_t BH, float* out, void* stream) {

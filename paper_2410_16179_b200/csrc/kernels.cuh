@@ -83,4 +83,39 @@ int launch_collision_counts(const uint32_t* qbits, const uint32_t* codes, int64_
                             int64_t n_local, int K, int L, int KLw, int KLq, int64_t nchunks, uint16_t* counts,
                             cudaStream_t st);
 
+// ---- decode v6: Query (dense scan6 or bucketed bucket_mark) -> S bitmaps -> estimator (attend)
+struct ScanArgs {
+    const uint32_t* qbits;
+    const uint32_t* codes;
+    uint32_t* sbits;              // [B][Hq][ceil(n/32)]
+    int64_t B, Hkv, Hq, n_local, nchunks, tiles;
+    int K, L, KL, KLw, KLq, ngroups, minc;
+    int nsw, depth, off_qx, off_qbw, off_part;  // set by scan6_layout
+};
+size_t scan6_layout(ScanArgs& a, int G, int max_smem);
+int launch_scan6(const ScanArgs& a, int nsm, int max_smem, cudaStream_t st);
+
+struct AttendArgs {
+    const uint16_t* q;
+    const float* center;
+    const float* key_norm;
+    const uint16_t* k;
+    const uint16_t* v;
+    const uint32_t* sbits;        // [B][Hq][ceil(n/32)]
+    int64_t B, Hkv, Hq, n_local, seq_offset, n_global;
+    int64_t nchunks, nstatic, tiles;
+    int K, L, minc, sink, local;
+    int off_wbuf, off_comb;       // set by attend_layout
+    float* out;
+    float* partial;
+    int32_t* s_count;
+    uint32_t* s_mask;             // debug: S_g restricted to D
+    uint32_t* weighted;           // debug: (head, key) pairs that received a finite weight (S_g u T)
+    uint32_t* unit_ctr;
+    float* parts;
+    uint32_t* status;
+};
+size_t attend_layout(AttendArgs& a, int G);
+int launch_attend(const AttendArgs& a, int nsm, int max_smem, cudaStream_t st);
+
 }  // namespace mp

@@ -20,16 +20,18 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-3
 
 
-@pytest.fixture(params=[5, 4], ids=["k5", "k4"], autouse=True)
+@pytest.fixture(params=[6, 5], ids=["k6", "k5"], autouse=True)
 def decode_kernel(request):
-    """Every parity test runs on both decode kernels (persistent warp-specialised
-    and cluster-per-chunk); they must agree with the oracle independently."""
+    """Every parity test runs on two decode paths: 6 = Query kernel + estimator kernel (the
+    default) and 5 = the persistent fused kernel (which falls back to the cluster-per-chunk
+    kernel 4 when its shared memory does not fit); they must agree with the oracle
+    independently."""
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device (no fallback)")
     pkg = _pkg()
     pkg.binding.set_decode_kernel(request.param)
     yield request.param
-    pkg.binding.set_decode_kernel(5)
+    pkg.binding.set_decode_kernel(6)
 
 
 def _dev():
@@ -358,3 +360,41 @@ def test_decode_session_graph_matches_decode():
         got = sess.step()
         torch.cuda.synchronize()
         assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("G,buckets", [(4, False), (4, True), (8, False), (1, True)])
+def test_weighted_set_is_s_union_t(G, buckets, decode_kernel):
+    """The compacted list the estimator gathers, exported as the (head, key) pairs that received a
+    finite weight: it must equal S_g u T exactly (oracle), and S_g restricted to D must equal the
+    oracle's S_g (Alg. 1)."""
+    if decode_kernel != 6:
+        pytest.skip("weighted-set export exists on the v6 path")
+    pkg = _pkg()
+    n = 5000
+    wl = synth.Workload("wset", 960 + G + 10 * buckets, B=2, Hq=2 * G, Hkv=2, n=n, K=8, L=40, sink=4, local=64)
+    k, v, q = synth.make_batch(wl)
+    W = synth.make_projections(wl.K, wl.L, wl.mips)
+    tk, tv, tq = _bf(k), _bf(v), _bf(q)
+    tW = torch.from_numpy(W).to(_dev())
+    mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, buckets=buckets).build(tk)
+    nw = (n + 31) // 32
+    sm = torch.zeros((2, wl.Hq, nw), dtype=torch.int32, device=_dev())
+    wt = torch.zeros((2, wl.Hq, nw), dtype=torch.int32, device=_dev())
+    out = torch.zeros((2, wl.Hq, 128), dtype=torch.float32, device=_dev())
+    ws = mp.decode_workspace(2, wl.Hq, 2, n, _dev())
+    pkg.binding.debug_decode_sets(mp.cfg, tq, None if buckets else mp.buf.codes, mp.buf.tables if buckets else None,
+                                  mp.buf.center, mp.buf.key_norm, tk, tv, 0, n, tW, ws, out, sm, wt)
+    torch.cuda.synchronize()
+    smn = sm.cpu().numpy().view(np.uint32)
+    wtn = wt.cpu().numpy().view(np.uint32)
+    refs = oracle.decode_batch(k, v, q, W, wl.K, wl.L, 1, 1, 2, 4, 64)
+    for b in range(2):
+        for h in range(2):
+            ref = refs[b][h]
+            for g in range(G):
+                row = h * G + g
+                s_bits = np.unpackbits(smn[b, row].view(np.uint8), bitorder="little")[:n]
+                w_bits = np.unpackbits(wtn[b, row].view(np.uint8), bitorder="little")[:n]
+                np.testing.assert_array_equal(s_bits, (ref["in_s"][g] == 1).astype(np.uint8))
+                np.testing.assert_array_equal(w_bits, (ref["in_s"][g] >= 1).astype(np.uint8))
+                assert _rel_err(out.cpu().numpy()[b, row], ref["out"][g]) <= TOL

@@ -215,6 +215,19 @@ int magicpig_decode_buckets_encoded(const magicpig_config* cfg, const uint16_t* 
  * (fixed order j = 0..P-1, so every rank gets bit-identical results). */
 int magicpig_merge_partials(const float* parts, int P, int64_t BH, float* out, void* stream);
 
+/* One whole decode step from HOST memory (the serving call): copies q_host
+ * [B][Hq][128] bf16 [host; pinned memory makes the copy asynchronous] into the
+ * workspace, encodes it, decodes it over the dense codes (tables ==
+ * NULL) or the bucketed tables (codes ignored) as magicpig_decode /
+ * magicpig_decode_buckets do (unsharded: seq_offset 0, n_global = n_local),
+ * copies the output to out_host [B][Hq][128] fp32 [host] and synchronizes
+ * `stream`, so out_host is valid when the call returns.  Returns 0 or an error
+ * code. */
+int magicpig_decode_host(const magicpig_config* cfg, const uint16_t* q_host, int64_t Hq, const uint32_t* codes,
+                         const int32_t* tables, const float* center, const float* key_norm, const uint16_t* k,
+                         const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local, const float* W, float* out_host,
+                         void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- debug ---
  * Canonical codes [B][Hkv][n][L] uint16, bit b of table t = column t*K+b. */
 int magicpig_export_codes(const magicpig_config* cfg, const uint32_t* codes, int64_t B, int64_t Hkv,
@@ -265,6 +278,33 @@ int magicpig_debug_decode_sets(const magicpig_config* cfg, const uint16_t* q, in
                                const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local, int64_t seq_offset,
                                int64_t n_global, const float* W, float* out, uint32_t* s_mask, uint32_t* weighted,
                                void* ws, size_t ws_bytes, void* stream);
+
+/* Debug: selected stages of a decode step (decode kernel 6 or 7, unsharded), for
+ * timing the kernels of the step separately.  `stage` is a bit mask:
+ *   1  Query(HT, q_code) (Alg. 1): the dense scan of `codes`, or the
+ *      bucketed `tables` if non-NULL -> per-head S bitmaps in the workspace;
+ *   2  (kernel 7) select: S_g restricted to D, union over the unit's heads,
+ *      ordered lists in the workspace;
+ *   4  the estimator over what the earlier stages left in the
+ *      workspace -> out (kernel 6: bits 2 and 4 both mean its one kernel).
+ * 7 = a whole decode step.  The query codes must already be in the workspace
+ * (magicpig_encode_queries).  Returns 0 or an error code (MAGICPIG_EINVAL for
+ * another kernel version). */
+int magicpig_debug_decode_stage(const magicpig_config* cfg, int stage, const uint16_t* q, int64_t Hq,
+                                const uint32_t* codes, const int32_t* tables, const float* center,
+                                const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
+                                int64_t n_local, float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Debug: magicpig_build_index (unsharded) with a CUDA event (cudaEvent_t, created
+ * by the caller) recorded on `stream` at each phase boundary: events[0] before the
+ * key statistics, [1] after them, [2] after the key norms / centering
+ * vector / MIPS radius, [3] after the operand preparation (xbar tiles),
+ * [4] after the hash GEMM and its exact fix-up.  Same results as
+ * magicpig_build_index. */
+int magicpig_debug_build_phases(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,
+                                const float* W, float* center, int64_t* r2, uint32_t* codes, float* key_norm,
+                                int64_t* key_sum, int64_t* count, void* ws, size_t ws_bytes, void* stream,
+                                void* const* events);
 
 /* Selects the decode kernel for subsequent decode calls of this process (a debug
  * knob for A/B measurement; default 6): 6 = Query kernel (dense code scan, or the

@@ -70,6 +70,10 @@ _SIGS = {
     "magicpig_debug_hash_acc": ([_p, _p, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_decode_timeline": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _p,
                                         _sz, _p], _i64),
+    "magicpig_decode_host": ([_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _sz, _p], _i),
+    "magicpig_debug_decode_stage": ([_p, _i, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _sz, _p],
+                                    _i),
+    "magicpig_debug_build_phases": ([_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p, _p], _i),
     "magicpig_strerror": ([_i], C.c_char_p),
     "magicpig_version": ([], C.c_char_p),
     "magicpig_launch_count": ([], C.c_uint64),
@@ -78,16 +82,17 @@ _SIGS = {
 _lib = None
 
 
-def lib(load_only: bool = True):
-    """Load the in-tree shared library (building it only if it is missing, or
-    if stale when load_only=False)."""
+def lib():
+    """Load the in-tree shared library, (re)building it first if it is missing
+    or older than its sources (so a kernel edit is never validated or timed
+    against a stale binary)."""
     global _lib
     if _lib is None:
         path = _build.LIB
         alt = os.environ.get("MAGICPIG_LIB")  # debug: A/B against another build of the library
         if alt:
             path = alt
-        elif not os.path.exists(path) or not load_only:
+        elif _build._stale():
             path = _build.build()
         L = C.CDLL(path)
         for name, (args, res) in _SIGS.items():
@@ -247,6 +252,20 @@ def decode_encoded(cfg, q, codes, center, key_norm, k, v, seq_offset, n_global, 
            "decode_encoded")
 
 
+def decode_host(cfg, q_host, codes, tables, center, key_norm, k, v, W, out_host, ws):
+    """One decode step from host memory: q_host [B][Hq][128] bf16 and out_host [B][Hq][128] fp32 are CPU
+    tensors (pinned for asynchronous copies); returns after out_host holds the result."""
+    B, Hkv, n, _ = k.shape
+    Hq = q_host.shape[1]
+    if q_host.is_cuda or out_host.is_cuda or q_host.dtype != torch.bfloat16 or out_host.dtype != torch.float32:
+        raise MagicPIGError("decode_host takes CPU tensors: q_host bf16, out_host float32")
+    if not (q_host.is_contiguous() and out_host.is_contiguous()) or tuple(out_host.shape) != (B, Hq, 128):
+        raise MagicPIGError("decode_host: contiguous q_host [B][Hq][128] and out_host [B][Hq][128]")
+    _check(lib().magicpig_decode_host(_cfg(cfg), C.c_void_p(q_host.data_ptr()), Hq, _ptr(codes), _ptr(tables),
+                                      _ptr(center), _ptr(key_norm), _ptr(k), _ptr(v), B, Hkv, n, _ptr(W),
+                                      C.c_void_p(out_host.data_ptr()), _ptr(ws), ws.numel(), _stream()), "decode_host")
+
+
 def merge_partials(parts, out):
     P, BH, _ = parts.shape
     _check(lib().magicpig_merge_partials(_ptr(parts), P, BH, _ptr(out), _stream()), "merge_partials")
@@ -303,6 +322,27 @@ def debug_decode_sets(cfg, q, codes, tables, center, key_norm, k, v, seq_offset,
                                             _ptr(key_norm), _ptr(k), _ptr(v), B, Hkv, n, seq_offset, n_global, _ptr(W),
                                             _ptr(out), _ptr(s_mask), _ptr(weighted), _ptr(ws), ws.numel(), _stream()),
            "debug_decode_sets")
+
+
+def debug_decode_stage(cfg, stage, q, codes, tables, center, key_norm, k, v, ws, out=None):
+    """Debug: stage 1 = the Query kernel alone (S bitmaps into ws), stage 2 = the estimator kernel alone."""
+    B, Hkv, n, _ = k.shape
+    Hq = q.shape[1]
+    _check(lib().magicpig_debug_decode_stage(_cfg(cfg), int(stage), _ptr(q), Hq, _ptr(codes), _ptr(tables),
+                                             _ptr(center), _ptr(key_norm), _ptr(k), _ptr(v), B, Hkv, n, _ptr(out),
+                                             _ptr(ws), ws.numel(), _stream()), "debug_decode_stage")
+
+
+def debug_build_phases(cfg, k, W, center, r2, codes, key_norm, key_sum, count, ws, events):
+    """build_index with torch.cuda.Event objects (5, enable_timing) recorded at the phase boundaries:
+    stats | norms | prep | hash GEMM + fix-up."""
+    B, Hkv, n, _ = k.shape
+    for e in events:  # torch creates the CUDA event lazily, on its first record
+        e.record()
+    arr = (C.c_void_p * 5)(*[C.c_void_p(e.cuda_event) for e in events])
+    _check(lib().magicpig_debug_build_phases(_cfg(cfg), _ptr(k), B, Hkv, n, _ptr(W), _ptr(center), _ptr(r2),
+                                             _ptr(codes), _ptr(key_norm), _ptr(key_sum), _ptr(count), _ptr(ws),
+                                             ws.numel(), _stream(), arr), "debug_build_phases")
 
 
 def set_decode_kernel(version: int):

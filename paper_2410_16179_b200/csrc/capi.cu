@@ -38,7 +38,7 @@ static int max_smem_optin() {
 // scan6 or bucket_mark) -> S bitmaps -> estimator kernel (attend.cu) (default); 5 = persistent
 // warp-specialised fused kernel (falls back to 4 when its shared memory does not fit), 4 = one
 // cluster per chunk.  5 and 4 are kept as A/B arms; all compute the same S bit for bit.
-static std::atomic<int> g_decode_kernel{6};
+static std::atomic<int> g_decode_kernel{7};
 
 static bool cfg_ok(const magicpig_config* c) {
     if (!c) return false;
@@ -126,6 +126,11 @@ struct DecodeWs {
     float* parts;
     int32_t* chunk_cnt;
     uint32_t* sbits;
+    uint32_t* ents;
+    int32_t* ucnt;
+    int32_t* hcnt;
+    uint16_t* qstage;  // magicpig_decode_host: q copied from the host
+    float* ostage;     //                       out before the copy to the host
     size_t bytes;
 };
 
@@ -150,10 +155,15 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     const int64_t nT = n_local < (int64_t)c->sink + c->local ? n_local : (int64_t)c->sink + c->local;
     const int64_t nst = nT > 0 ? (nT + KCHUNK - 1) / KCHUNK : 1;
     const size_t parts4 = (size_t)units * (nch + nst) * 8 * G * PART * 4;      // up to 8 CTAs per cluster
-    const size_t parts5 = (size_t)(units + num_sms()) * G * PREC5 * 4;         // record u + CTA
+    const size_t parts5 = (size_t)(units + (int64_t)num_sms() * EST_WARPS) * G * PREC5 * 4;  // record u + warp
     w.parts = (float*)take(parts4 > parts5 ? parts4 : parts5);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
-    w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4);  // bucket mode S bitmaps
+    w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4);  // S bitmaps of the Query step
+    w.ents = (uint32_t*)take((size_t)units * (n_local > 0 ? n_local : 1) * 4);  // v7 unit lists
+    w.ucnt = (int32_t*)take((size_t)units * 4);
+    w.hcnt = (int32_t*)take((size_t)B * Hq * 4);
+    w.qstage = (uint16_t*)take((size_t)B * Hq * HD * 2);
+    w.ostage = (float*)take((size_t)B * Hq * HD * 4);
     w.bytes = off;
     return w;
 }
@@ -270,7 +280,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
                        int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
                        float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
                        void* stream, unsigned long long* timeline, int64_t timeline_len, int64_t* grid_out,
-                       const int32_t* tables = nullptr, uint32_t* weighted = nullptr) {
+                       const int32_t* tables = nullptr, uint32_t* weighted = nullptr, int stages = 7) {
     if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
     if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
     const int64_t G = Hq / Hkv;
@@ -347,10 +357,11 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
     const int kver = g_decode_kernel.load();
-    if (kver % 10 == 6 && !timeline) {
+    if ((kver % 10 == 6 || kver % 10 == 7) && !timeline) {
         // Query(HT, q_code) -> S bitmaps: bucketed tables or the dense code scan (PDL after the encode)
-        int rc;
-        if (tables) {
+        int rc = 0;
+        if (!(stages & 1)) {
+        } else if (tables) {
             rc = launch_bucket_mark(w.qbits, tables, B, Hq, Hkv, n_local, cfg->K, cfg->L, g.KLw,
                                     cfg->min_collisions, w.sbits, st);
         } else {
@@ -365,7 +376,23 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
             sa.minc = cfg->min_collisions;
             rc = launch_scan6(sa, num_sms(), max_smem_optin(), st);
         }
-        if (rc) return rc;
+        if (rc || !(stages & 6)) return rc;
+        if (kver % 10 == 7 && B * Hkv <= EST_MAX_UNITS && n_local < (1 << 24)) {
+            // ordered S_g u ... lists per unit, then the balanced estimator
+            EstArgs ea;
+            memset(&ea, 0, sizeof(ea));
+            ea.q = q, ea.center = center, ea.key_norm = key_norm, ea.k = k, ea.v = v, ea.sbits = w.sbits;
+            ea.B = B, ea.Hkv = Hkv, ea.Hq = Hq, ea.n_local = n_local, ea.seq_offset = seq_offset;
+            ea.n_global = n_global, ea.nchunks = g.nchunks;
+            ea.K = cfg->K, ea.L = cfg->L, ea.minc = cfg->min_collisions, ea.sink = cfg->sink, ea.local = cfg->local;
+            ea.ents = w.ents, ea.ucnt = w.ucnt, ea.hcnt = w.hcnt, ea.s_mask = s_mask, ea.weighted = weighted;
+            ea.out = out, ea.partial = partial, ea.s_count = s_count;
+            ea.unit_ctr = w.unit_ctr, ea.parts = w.parts, ea.status = w.status;
+            if (grid_out) *grid_out = num_sms();
+            if (stages & 2) rc = launch_select(ea, st);
+            if (rc || !(stages & 4)) return rc;
+            return launch_estimate(ea, num_sms(), max_smem_optin(), st);
+        }
         // estimator over S_g u T
         AttendArgs aa;
         memset(&aa, 0, sizeof(aa));
@@ -379,7 +406,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
         if (grid_out) *grid_out = aa.tiles < num_sms() ? aa.tiles : num_sms();
         return launch_attend(aa, num_sms(), max_smem_optin(), st);
     }
-    if (weighted) return MAGICPIG_EINVAL;  // the weighted-set export exists on the v6 path only
+    if (weighted || stages != 7) return MAGICPIG_EINVAL;  // v6 / v7 paths only
     bool v5 = kver % 10 == 5 || tables;  // bucket mode runs on the persistent kernel only
     a.dbg = kver / 10;
     if (v5) {
@@ -405,7 +432,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
 }
 
 extern "C" int magicpig_debug_set_decode_kernel(int version) {
-    if (version % 10 != 4 && version % 10 != 5 && version % 10 != 6) return MAGICPIG_EINVAL;
+    if (version % 10 < 4 || version % 10 > 7) return MAGICPIG_EINVAL;
     g_decode_kernel.store(version);
     return MAGICPIG_OK;
 }
@@ -490,13 +517,77 @@ int magicpig_debug_decode_sets(const magicpig_config* cfg, const uint16_t* q, in
                                void* ws, size_t ws_bytes, void* stream) {
     if (!W || !weighted || (n_local > 0 && !codes && !tables) || n_local < 1) return MAGICPIG_EINVAL;
     if (!cfg_ok(cfg) || Hq < Hkv || Hkv < 1 || B < 1 || Hq % Hkv) return MAGICPIG_EINVAL;
-    if (g_decode_kernel.load() % 10 != 6) return MAGICPIG_EINVAL;
+    if (g_decode_kernel.load() % 10 < 6) return MAGICPIG_EINVAL;
     if (cudaMemsetAsync(weighted, 0, (size_t)B * Hq * ((n_local + 31) / 32) * 4, S(stream)) != cudaSuccess)
         return MAGICPIG_ECUDA;
     int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
     if (rc) return rc;
     return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
                        nullptr, nullptr, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, weighted);
+}
+
+int magicpig_decode_host(const magicpig_config* cfg, const uint16_t* q_host, int64_t Hq, const uint32_t* codes,
+                         const int32_t* tables, const float* center, const float* key_norm, const uint16_t* k,
+                         const uint16_t* v, int64_t B, int64_t Hkv, int64_t n_local, const float* W, float* out_host,
+                         void* ws, size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || !q_host || !out_host || !W || !ws || B < 1 || Hkv < 1 || Hq < Hkv || Hq % Hkv || n_local < 0)
+        return MAGICPIG_EINVAL;
+    if (tables && !buckets_ok(cfg, n_local)) return MAGICPIG_EINVAL;
+    DecodeWs w = decode_layout(cfg, B, Hq, Hkv, n_local, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    cudaStream_t st = S(stream);
+    if (cudaMemcpyAsync(w.qstage, q_host, (size_t)B * Hq * HD * 2, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return MAGICPIG_ECUDA;
+    int rc = MAGICPIG_OK;
+    if (n_local > 0) rc = magicpig_encode_queries(cfg, w.qstage, B, Hq, W, ws, ws_bytes, stream);
+    if (rc) return rc;
+    rc = decode_impl(cfg, w.qstage, Hq, tables ? nullptr : codes, center, key_norm, k, v, B, Hkv, n_local, 0, n_local,
+                     w.ostage, nullptr, nullptr, nullptr, ws, ws_bytes, stream, nullptr, 0, nullptr, tables);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(out_host, w.ostage, (size_t)B * Hq * HD * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return MAGICPIG_ECUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? MAGICPIG_OK : MAGICPIG_ECUDA;
+}
+
+int magicpig_debug_decode_stage(const magicpig_config* cfg, int stage, const uint16_t* q, int64_t Hq,
+                                const uint32_t* codes, const int32_t* tables, const float* center,
+                                const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
+                                int64_t n_local, float* out, void* ws, size_t ws_bytes, void* stream) {
+    if (stage < 1 || stage > 7) return MAGICPIG_EINVAL;
+    if (g_decode_kernel.load() % 10 < 6 || n_local < 1) return MAGICPIG_EINVAL;
+    return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, 0, n_local, out, nullptr, nullptr,
+                       nullptr, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, nullptr, stage);
+}
+
+int magicpig_debug_build_phases(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,
+                                const float* W, float* center, int64_t* r2, uint32_t* codes, float* key_norm,
+                                int64_t* key_sum, int64_t* count, void* ws, size_t ws_bytes, void* stream,
+                                void* const* events) {
+    if (!events || n < 1) return MAGICPIG_EINVAL;
+    for (int i = 0; i < 5; i++)
+        if (!events[i]) return MAGICPIG_EINVAL;
+    cudaStream_t st = S(stream);
+    auto rec = [&](int i) { return cudaEventRecord((cudaEvent_t)events[i], st) == cudaSuccess; };
+    if (!rec(0)) return MAGICPIG_ECUDA;
+    int rc = magicpig_key_stats(cfg, k, B, Hkv, n, 0, n, key_sum, count, ws, ws_bytes, stream);
+    if (rc) return rc;
+    if (!rec(1)) return MAGICPIG_ECUDA;
+    rc = magicpig_key_norms(cfg, k, B, Hkv, n, 0, n, key_sum, count, center, r2, ws, ws_bytes, stream);
+    if (rc) return rc;
+    if (!rec(2)) return MAGICPIG_ECUDA;
+    if (!cfg_ok(cfg) || !W || !codes || !key_norm) return MAGICPIG_EINVAL;
+    BuildWs w = build_layout(cfg, B, Hkv, n, ws);
+    if (ws_bytes < w.bytes) return MAGICPIG_EWORKSPACE;
+    const Geom g = make_geom(cfg->K, cfg->L, n);
+    if (cudaMemsetAsync(w.fix_count, 0, 4, st) != cudaSuccess) return MAGICPIG_ECUDA;
+    rc = launch_prep(k, B * Hkv, n, w.n_pad, cfg->mips, w.KD, center, r2, w.xt, w.xnorm, key_norm, W, g.KL, w.NT,
+                     w.wt, w.wmax, w.status, st);
+    if (rc) return rc;
+    if (!rec(3)) return MAGICPIG_ECUDA;
+    rc = launch_hash_gemm(w.xt, w.wt, w.xnorm, w.wmax, codes, w.fix_list, w.fix_count, w.fix_cap, B * Hkv, n, w.n_pad,
+                          g.nchunks, w.KD, g.KL, w.NT, g.KLq, w.status, nullptr, st);
+    if (rc) return rc;
+    return rec(4) ? MAGICPIG_OK : MAGICPIG_ECUDA;
 }
 
 int magicpig_merge_partials(const float* parts, int P, int64_t BH, float* out, void* stream) {

@@ -1,0 +1,801 @@
+// estimate.cu -- the sampling-and-estimation half of a MagicPIG decode step
+// (Algorithm 1), after the Query step has produced per-head
+// S bitmaps (dense code scan, scan6.cu, or the bucketed tables, buckets.cu):
+//
+//   select_kernel    CTA per (sequence, kv head) unit: S_g restricted to the
+//                    dynamic keys D (P:171 static cache excluded), the union over
+//                    the G query heads of the unit, compacted in ascending key
+//                    order into one list per unit (entry = key | head bits << 24),
+//                    plus |S_g| per head and the list length.
+//   estimate_kernel  the self-normalised importance-sampling estimator
+//                        o_g = sum_{i in S_g u T} e^{z_i} v_i / sum e^{z_i},
+//                        z_i = q_g.k_i / sqrt(d) - ln u_i      (u_i = 1 on T)
+//                    with u_i the closed-form sampling probability (Eq. P:86-91)
+//                    at the angle between the hashed vectors (reading R5).
+//                    The unit lists (each preceded by the unit's static keys T,
+//                    P:619) are concatenated; every warp of the persistent grid
+//                    owns one contiguous range of that sequence (perfect balance,
+//                    no producer warp), cut into 16-row slabs at unit boundaries.
+//                    Per slab: K and V rows by one 256-B bulk copy each
+//                    (cp.async.bulk, completion on a per-stage mbarrier, two
+//                    stages per warp, entries of the next slab prefetched),
+//                    logits q.k and hashed dots qbar.xbar on tensor cores
+//                    (mma.sync bf16, xbar = bf16(fl32(k - c)) formed in the A
+//                    fragments), ln u for the (row, head) items in S only
+//                    (compacted over the warp), online softmax (rescale skipped
+//                    when no running max moves), a[g][d] += w v on tensor cores
+//                    with w split into bf16 hi + lo (fp32-accurate).
+//                    When a warp leaves a unit it writes its record (m, s, a) to
+//                    parts[u + warp]; the last warp of the unit (acq_rel counter)
+//                    merges the unit's records in warp order (log-sum-exp,
+//                    "recursive attention").  Counters self-clean, so the
+//                    step is CUDA-graph replayable.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mp {
+namespace v7 {
+
+constexpr int SEL_WARPS = 16;  // select CTA
+constexpr int CPW = 4;         // chunks per select warp per round
+constexpr int NW = EST_WARPS;  // estimator warps per CTA
+constexpr int SR = 16;         // rows per slab (mma M)
+constexpr int NST = 2;         // row stages per warp
+constexpr int SPW = 2;         // minimum slabs per active warp
+constexpr int RP = 272;        // shared-memory row pitch (256 B + 16: ldmatrix conflict-free)
+constexpr int PREC = PREC5;    // record per head: m, s, 0, 0, a[128]
+constexpr int MB = 16;         // unit merge: records per load round
+constexpr float INV_SQRT_D = 0.08838834764831845f;
+
+struct __align__(128) WBuf {
+    uint8_t k[NST][SR * RP];  // K rows
+    uint8_t v[NST][SR * RP];  // V rows
+    float xn[NST][SR];        // |xbar_i|
+    float c[HD];              // centering vector of the warp's current unit (16-B aligned: float4 stores)
+    float items[SR * 8];      // compacted (row, head) items: cos in, ln u out
+    uint16_t wt[16 * SR];     // PV B operand: [column n][row] bf16 (hi | lo weights)
+    int key[NST][SR];         // local key index of each row
+    uint32_t bits[NST][SR];   // bit g: key in S_g; 0x100: static (u = 1)
+    uint64_t bar[NST];        // stage barriers: bulk-copy bytes + the lanes' cp.async (norms)
+    long long su[NST];        // unit of the slab in the stage
+    int snr[NST];             // rows of the slab
+};
+static_assert(offsetof(WBuf, c) % 16 == 0 && offsetof(WBuf, wt) % 16 == 0 && offsetof(WBuf, bar) % 8 == 0,
+              "WBuf alignment");
+
+__device__ __forceinline__ void cp4z(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+// D(16x8 fp32) += A(16x16 bf16, row) * B(16x8 bf16, col): exact products, fp32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// bf16 pair (lo = element c, hi = element c+1) -> bf16(fl32(k - c)) pair (cvt.rn.bf16x2)
+__device__ __forceinline__ uint32_t xbar_pair(uint32_t kw, float c0, float c1) {
+    const __nv_bfloat162 xb = __floats2bfloat162_rn(__fsub_rn(__uint_as_float(kw << 16), c0),
+                                                    __fsub_rn(__uint_as_float(kw & 0xffff0000u), c1));
+    return *reinterpret_cast<const uint32_t*>(&xb);
+}
+__device__ __forceinline__ uint32_t range_mask(int64_t base, int64_t lo, int64_t hi) {
+    int64_t x = lo - base, y = hi - base;
+    x = x < 0 ? 0 : (x > 32 ? 32 : x);
+    y = y < 0 ? 0 : (y > 32 ? 32 : y);
+    if (y <= x) return 0u;
+    const uint32_t hiMask = y >= 32 ? 0xffffffffu : ((1u << y) - 1u);
+    const uint32_t loMask = x >= 32 ? 0xffffffffu : ((1u << x) - 1u);
+    return hiMask & ~loMask;
+}
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, v, m);
+        if (lane >= m) v += x;
+    }
+    return v;
+}
+
+// static keys T on this shard (sink tokens at global [0, sink), local window at [n - local, n)),
+// as local index ranges [lo1, lo1 + len1) u [lo2, lo2 + len2)
+struct StaticRanges {
+    int64_t lo1, len1, lo2, len2;
+};
+__device__ __forceinline__ StaticRanges static_ranges(const EstArgs& a) {
+    StaticRanges r;
+    const int64_t off = a.seq_offset, nl = a.n_local;
+    r.lo1 = max((int64_t)0, -off);
+    const int64_t hi1 = min(nl, (int64_t)a.sink - off);
+    r.len1 = hi1 > r.lo1 ? hi1 - r.lo1 : 0;
+    r.lo2 = max((int64_t)0, a.n_global - a.local - off);
+    const int64_t hi2 = min(nl, a.n_global - off);
+    if (r.len1 > 0 && r.lo2 < hi1) r.lo2 = hi1;
+    r.len2 = hi2 > r.lo2 ? hi2 - r.lo2 : 0;
+    return r;
+}
+
+// ============================================================================ select
+template <int G>
+__global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(EstArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ int wtot[SEL_WARPS];
+    __shared__ int hsum[SEL_WARPS][8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t u = blockIdx.x, b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
+    const int64_t nwb = (a.n_local + 31) >> 5;
+    const StaticRanges sr = static_ranges(a);
+    uint32_t* ents = a.ents + u * a.n_local;
+    int hc[G];
+#pragma unroll
+    for (int g = 0; g < G; g++) hc[g] = 0;
+    int64_t run = 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // S bitmaps of the Query kernel
+#pragma unroll 1
+    for (int64_t r0 = 0; r0 < a.nchunks; r0 += SEL_WARPS * CPW) {
+        uint32_t sg[CPW][G];
+#pragma unroll
+        for (int j = 0; j < CPW; j++) {
+            const int64_t wi = (r0 + warp * CPW + j) * 32 + lane;
+            const bool ok = r0 + warp * CPW + j < a.nchunks && wi < nwb;
+#pragma unroll
+            for (int g = 0; g < G; g++) sg[j][g] = ok ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
+        }
+        int cex[CPW], ctot[CPW], wt = 0;
+#pragma unroll
+        for (int j = 0; j < CPW; j++) {
+            const int64_t wi = (r0 + warp * CPW + j) * 32 + lane;
+            const int64_t base = wi * 32;
+            const uint32_t dmask = range_mask(base, 0, a.n_local) &
+                                   ~(range_mask(base, sr.lo1, sr.lo1 + sr.len1) |
+                                     range_mask(base, sr.lo2, sr.lo2 + sr.len2));
+            uint32_t un = 0u;
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                sg[j][g] &= dmask;
+                un |= sg[j][g];
+                hc[g] += __popc(sg[j][g]);
+            }
+            if (a.s_mask && r0 + warp * CPW + j < a.nchunks && wi < nwb) {
+#pragma unroll
+                for (int g = 0; g < G; g++) a.s_mask[(qh0 + g) * nwb + wi] = sg[j][g];
+            }
+            const int c = __popc(un);
+            const int incl = warp_incl_scan(c, lane);
+            cex[j] = wt + incl - c;
+            ctot[j] = __shfl_sync(0xffffffffu, incl, 31);
+            wt += ctot[j];
+        }
+        if (lane == 0) wtot[warp] = wt;
+        __syncthreads();
+        int woff = 0, rtot = 0;
+#pragma unroll
+        for (int w = 0; w < SEL_WARPS; w++) {
+            const int x = wtot[w];
+            woff += w < warp ? x : 0;
+            rtot += x;
+        }
+#pragma unroll
+        for (int j = 0; j < CPW; j++) {
+            const int64_t base = ((r0 + warp * CPW + j) * 32 + lane) * 32;
+            uint32_t un = 0u;
+#pragma unroll
+            for (int g = 0; g < G; g++) un |= sg[j][g];
+            int64_t pos = run + woff + cex[j];
+            while (un) {
+                const int bit = __ffs(un) - 1;
+                un &= un - 1u;
+                uint32_t hb = 0u;
+#pragma unroll
+                for (int g = 0; g < G; g++) hb |= ((sg[j][g] >> bit) & 1u) << g;
+                ents[pos++] = (uint32_t)(base + bit) | (hb << 24);
+            }
+        }
+        run += rtot;
+        __syncthreads();  // wtot reusable
+    }
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+        int c = hc[g];
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+        if (lane == 0) hsum[warp][g] = c;
+    }
+    __syncthreads();
+    if (tid < G) {
+        int c = 0;
+#pragma unroll
+        for (int w = 0; w < SEL_WARPS; w++) c += hsum[w][tid];
+        a.hcnt[qh0 + tid] = c;
+    }
+    if (tid == 0) a.ucnt[u] = (int32_t)run;
+}
+
+// ============================================================================ estimate
+// owner warp of entry e when E entries are split into W contiguous ranges [k E / W, (k+1) E / W)
+__device__ __forceinline__ int64_t owner_of(int64_t e, int64_t E, int64_t W) { return ((e + 1) * W - 1) / E; }
+
+template <int G>
+__global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
+    constexpr int NT = (2 * G + 7) / 8;  // PV n-tiles: columns [hi heads | lo heads | pad]
+    extern __shared__ __align__(128) uint8_t dsm[];
+    int64_t* pref = reinterpret_cast<int64_t*>(dsm);  // [units + 1] first entry of each unit
+    __shared__ long long wsum[NW];
+    WBuf* wbuf = reinterpret_cast<WBuf*>(dsm + a.off_wbuf);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t units = a.B * a.Hkv;
+    const int64_t nwb = (a.n_local + 31) >> 5;
+    const StaticRanges sr = static_ranges(a);
+    const int64_t nT = sr.len1 + sr.len2;
+    WBuf& wb = wbuf[warp];
+
+    if (lane < NST) mbar_init(&wb.bar[lane], 33);  // 1 expect_tx + 32 noinc arrivals
+    // rows a slab does not load must hold finite values (0 * stale = 0); pad columns of the PV weights stay 0
+    for (int e = lane; e < (int)offsetof(WBuf, c) / 16; e += 32)
+        reinterpret_cast<uint4*>(&wb)[e] = make_uint4(0u, 0u, 0u, 0u);
+    for (int e = lane; e < 8 * SR; e += 32) reinterpret_cast<uint32_t*>(wb.wt)[e] = 0u;
+    fence_mbar_init();
+    fence_proxy_async();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // lists of the select kernel
+
+    // ---- unit prefix over the concatenated lists: unit u = its static keys, then its list
+    {
+        const int64_t per = (units + NW * 32 - 1) / (NW * 32);
+        const int64_t u0 = min(units, (int64_t)tid * per), u1 = min(units, u0 + per);
+        int64_t s = 0;
+        for (int64_t u = u0; u < u1; u++) s += nT + (int64_t)__ldcg(a.ucnt + u);
+        long long incl = s;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const long long x = __shfl_up_sync(0xffffffffu, incl, m);
+            if (lane >= m) incl += x;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int64_t off = 0;
+        for (int w = 0; w < warp; w++) off += wsum[w];
+        int64_t run = off + incl - s;
+        for (int64_t u = u0; u < u1; u++) {
+            pref[u] = run;
+            run += nT + (int64_t)__ldcg(a.ucnt + u);
+        }
+        if (tid == NW * 32 - 1) pref[units] = run;
+        __syncthreads();
+    }
+    const int64_t E = pref[units];
+    // units with no entry at all (S and T empty): zero output, degenerate status
+    if (blockIdx.x == 0) {
+        for (int64_t u = tid; u < units; u += NW * 32) {
+            if (pref[u + 1] != pref[u]) continue;
+            const int64_t b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
+            for (int g = 0; g < G; g++) {
+                const int64_t row = qh0 + g;
+                for (int d = 0; d < HD; d++) {
+                    if (a.out) a.out[row * HD + d] = 0.0f;
+                    if (a.partial) a.partial[row * PART + 2 + d] = 0.0f;
+                }
+                if (a.partial) a.partial[row * PART] = -INFINITY, a.partial[row * PART + 1] = 0.0f;
+                if (a.s_count) a.s_count[row] = a.hcnt[row];
+            }
+            if (a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
+        }
+    }
+    if (E == 0) return;
+    const int64_t Wt = (int64_t)gridDim.x * NW;
+    int64_t Wa = (E + SR * SPW - 1) / (SR * SPW);
+    Wa = Wa < 1 ? 1 : (Wa > Wt ? Wt : Wa);
+    const int64_t kw = (int64_t)warp * gridDim.x + blockIdx.x;  // active warps spread over the CTAs first
+    if (kw >= Wa) return;
+    const int64_t e_lo = kw * E / Wa, e_hi = (kw + 1) * E / Wa;
+    if (e_lo >= e_hi) return;
+
+    // ---------------------------------------------------------------- per-warp pipeline
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int h0 = 2 * t4, h1 = 2 * t4 + 1;  // logit-side heads of this thread (columns of the m16n8 D)
+    auto pv_head = [&](int nt, int i) {
+        const int n = nt * 8 + 2 * t4 + i;
+        return n < G ? n : (n < 2 * G ? n - G : -1);
+    };
+    auto find_unit = [&](int64_t e) {  // last u with pref[u] <= e (pref nondecreasing, pref[0] = 0)
+        int64_t lo = 0, hi = units;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (pref[mid] <= e) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+
+    // plan: the next slab to issue (unit, first entry, rows) with this lane's entry prefetched
+    int64_t pu = find_unit(e_lo), pcur = e_lo;
+    while (pref[pu + 1] <= pcur) pu++;
+    int p_nr = 0, p_key = 0;
+    uint32_t p_bits = 0u;
+    auto plan = [&]() {
+        if (pcur >= e_hi) {
+            p_nr = 0;
+            return;
+        }
+        while (pref[pu + 1] <= pcur) pu++;
+        const int64_t uend = min(e_hi, pref[pu + 1]);
+        p_nr = (int)min((int64_t)SR, uend - pcur);
+        const int r = lane & 15;
+        p_key = 0;
+        p_bits = 0u;
+        if (r < p_nr) {
+            const int64_t j = pcur - pref[pu] + r;
+            if (j < nT) {
+                p_key = (int)(j < sr.len1 ? sr.lo1 + j : sr.lo2 + (j - sr.len1));
+                p_bits = 0x100u | ((1u << G) - 1u);
+            } else {
+                const uint32_t e = __ldcg(a.ents + pu * a.n_local + (j - nT));
+                p_key = (int)(e & 0xffffffu);
+                p_bits = e >> 24;
+            }
+        }
+    };
+    int issued = 0, computed = 0;
+    auto issue = [&]() {
+        if (p_nr == 0) return;
+        const int st = issued % NST;
+        const int r = lane & 15;
+        const int nr = p_nr;
+        if (lane < 16) {
+            wb.key[st][r] = p_key;
+            wb.bits[st][r] = p_bits;
+        }
+        if (lane == 0) {
+            wb.su[st] = pu;
+            wb.snr[st] = nr;
+        }
+        uint64_t* bar = &wb.bar[st];
+        fence_proxy_async();  // this stage's earlier ldmatrix reads before the async-proxy refill
+        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)nr * 512u);
+        __syncwarp();
+        if (r < nr) {
+            const int64_t row = pu * a.n_local + p_key;
+            if (lane < 16) {
+                bulk_g2s(wb.k[st] + r * RP, a.k + row * HD, 256, bar);
+                cp4z(&wb.xn[st][r], a.key_norm + row, true);
+            } else {
+                bulk_g2s(wb.v[st] + r * RP, a.v + row * HD, 256, bar);
+            }
+        }
+        cp_mbar_arrive_noinc(bar);
+        issued++;
+        pcur += nr;
+        plan();
+    };
+
+    float acc[8][NT][4];
+    float m0 = -INFINITY, m1 = -INFINITY, s0 = 0.0f, s1 = 0.0f;
+    uint32_t qf[8][2];
+    float qn0 = 0.0f, qn1 = 0.0f;
+    auto reset_state = [&]() {
+#pragma unroll
+        for (int dt = 0; dt < 8; dt++)
+#pragma unroll
+            for (int nt = 0; nt < NT; nt++)
+                acc[dt][nt][0] = acc[dt][nt][1] = acc[dt][nt][2] = acc[dt][nt][3] = 0.0f;
+        m0 = m1 = -INFINITY;
+        s0 = s1 = 0.0f;
+    };
+    auto load_unit = [&](int64_t u) {
+        const int64_t b = u / a.Hkv, hkv = u % a.Hkv;
+        const int64_t qh0 = b * a.Hq + hkv * G;
+        float sq = 0.0f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ks++) {
+            const int d0 = 16 * ks + 2 * t4;
+            if (g4 < G) {
+                const uint32_t* qr = reinterpret_cast<const uint32_t*>(a.q + (qh0 + g4) * HD);
+                qf[ks][0] = __ldg(qr + d0 / 2);
+                qf[ks][1] = __ldg(qr + d0 / 2 + 4);
+            } else {
+                qf[ks][0] = qf[ks][1] = 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                const float lo = __uint_as_float(qf[ks][i] << 16), hi = __uint_as_float(qf[ks][i] & 0xffff0000u);
+                sq = fmaf(lo, lo, fmaf(hi, hi, sq));
+            }
+        }
+        __syncwarp();  // the previous unit's readers of wb.c are done
+        *reinterpret_cast<float4*>(&wb.c[4 * lane]) = __ldg(reinterpret_cast<const float4*>(a.center + u * HD) + lane);
+        __syncwarp();
+        // |q_g|^2: lanes 4g .. 4g+3 hold head g's 128 elements
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        const float qn = sqrtf(sq);
+        qn0 = __shfl_sync(0xffffffffu, qn, 4 * h0);
+        qn1 = __shfl_sync(0xffffffffu, qn, 4 * (h1 & 7));
+    };
+
+    // leave unit u: record (m, s, a) of this warp -> parts[u + kw]; the last warp of u merges
+    auto flush = [&](int64_t u) {
+        float* rec = a.parts + (size_t)(u + kw) * G * PREC;
+#pragma unroll
+        for (int dt = 0; dt < 8; dt++) {
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                // hi column of head h at (nt = 0, i); its lo column G + h
+                float hiA = acc[dt][0][i], hiB = acc[dt][0][2 + i], loA, loB;
+                if constexpr (G == 8) {
+                    loA = acc[dt][NT - 1][i];
+                    loB = acc[dt][NT - 1][2 + i];
+                } else if constexpr (G == 4) {
+                    loA = __shfl_down_sync(0xffffffffu, hiA, 2);
+                    loB = __shfl_down_sync(0xffffffffu, hiB, 2);
+                } else if constexpr (G == 2) {
+                    loA = __shfl_down_sync(0xffffffffu, hiA, 1);
+                    loB = __shfl_down_sync(0xffffffffu, hiB, 1);
+                } else {
+                    loA = acc[dt][0][1];
+                    loB = acc[dt][0][3];
+                }
+                const int h = 2 * t4 + i;
+                const bool own = (G == 1) ? (t4 == 0 && i == 0) : (h < G);
+                if (own) {
+                    __stcg(rec + h * PREC + 4 + dt * 16 + g4, hiA + loA);
+                    __stcg(rec + h * PREC + 4 + dt * 16 + g4 + 8, hiB + loB);
+                }
+            }
+        }
+        if (g4 == 0) {
+            if (h0 < G) __stcg(reinterpret_cast<float2*>(rec + h0 * PREC), make_float2(m0, s0));
+            if (h1 < G) __stcg(reinterpret_cast<float2*>(rec + h1 * PREC), make_float2(m1, s1));
+        }
+        __syncwarp();
+        const int64_t k_lo = owner_of(pref[u], E, Wa), k_hi = owner_of(pref[u + 1] - 1, E, Wa);
+        const uint32_t np = (uint32_t)(k_hi - k_lo + 1);
+        uint32_t old = 0;
+        if (lane == 0)
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.unit_ctr + u) : "memory");
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old != np - 1) return;
+        __syncwarp();
+        // last warp of the unit: merge records u + k_lo .. u + k_hi in fixed order, head by head
+        const float* pu0 = a.parts + (size_t)(u + k_lo) * G * PREC;
+        const int64_t b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
+        const int nrec = (int)np;
+#pragma unroll 1
+        for (int g = 0; g < G; g++) {
+            float M = -INFINITY, S = 0.0f;
+            float4 A = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll 1
+            for (int c0 = 0; c0 < nrec; c0 += MB) {
+                const int nr = min(MB, nrec - c0);
+                float4 av[MB];
+#pragma unroll
+                for (int jj = 0; jj < MB; jj++)
+                    av[jj] = jj < nr ? __ldcg(reinterpret_cast<const float4*>(pu0 + ((size_t)(c0 + jj) * G + g) * PREC +
+                                                                            4) +
+                                              lane)
+                                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                const float2 hd = lane < nr ? __ldcg(reinterpret_cast<const float2*>(pu0 + ((size_t)(c0 + lane) * G + g) *
+                                                                                              PREC))
+                                            : make_float2(-INFINITY, 0.0f);
+                float Mn = hd.x;
+#pragma unroll
+                for (int m = 16; m >= 1; m >>= 1) Mn = fmaxf(Mn, __shfl_xor_sync(0xffffffffu, Mn, m));
+                Mn = fmaxf(Mn, M);
+                const float fo = M == -INFINITY ? 0.0f : __expf(M - Mn);
+                const float fc = hd.x == -INFINITY ? 0.0f : __expf(hd.x - Mn);
+                S = S * fo + warp_sum_f(fc * hd.y);
+                A.x *= fo, A.y *= fo, A.z *= fo, A.w *= fo;
+#pragma unroll
+                for (int jj = 0; jj < MB; jj++) {
+                    const float fj = __shfl_sync(0xffffffffu, fc, jj);
+                    A.x = fmaf(fj, av[jj].x, A.x);
+                    A.y = fmaf(fj, av[jj].y, A.y);
+                    A.z = fmaf(fj, av[jj].z, A.z);
+                    A.w = fmaf(fj, av[jj].w, A.w);
+                }
+                M = Mn;
+            }
+            const int64_t row = qh0 + g;
+            if (a.out) {
+                const float inv = S > 0.0f ? 1.0f / S : 0.0f;
+                *reinterpret_cast<float4*>(a.out + row * HD + 4 * lane) = make_float4(A.x * inv, A.y * inv, A.z * inv,
+                                                                                      A.w * inv);
+            }
+            if (a.partial) {
+                float* pp = a.partial + row * PART;
+                *reinterpret_cast<float2*>(pp + 2 + 4 * lane) = make_float2(A.x, A.y);
+                *reinterpret_cast<float2*>(pp + 4 + 4 * lane) = make_float2(A.z, A.w);
+                if (lane == 0) pp[0] = M, pp[1] = S;
+            }
+            if (lane == 0) {
+                if (a.s_count) a.s_count[row] = __ldcg(a.hcnt + row);
+                if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
+            }
+        }
+        if (lane == 0) a.unit_ctr[u] = 0u;
+    };
+
+    plan();
+#pragma unroll 1
+    for (int i = 0; i < NST; i++) issue();
+    int64_t cur_u = -1;
+    reset_state();
+#pragma unroll 1
+    while (computed < issued) {
+        const int st = computed % NST;
+        const int64_t su = wb.su[st];
+        const int nr = wb.snr[st];
+        if (su != cur_u) {
+            if (cur_u >= 0) {
+                flush(cur_u);
+                reset_state();
+            }
+            cur_u = su;
+            load_unit(su);
+        }
+        mbar_wait(&wb.bar[st], (uint32_t)((computed / NST) & 1));
+        const uint8_t* Kt = wb.k[st];
+        const uint8_t* Vt = wb.v[st];
+
+        // (1) logits l = q.k and hashed dots qbar.xbar (mma.sync bf16, fp32 accumulate)
+        float dl[4] = {0.0f, 0.0f, 0.0f, 0.0f}, dx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        {
+            const int mi = lane >> 3, rr = lane & 7;
+            const int row = (mi & 1) * 8 + rr;
+            const uint32_t kbase = smem_u32(Kt + row * RP + (mi >> 1) * 16);
+#pragma unroll
+            for (int ks = 0; ks < 8; ks++) {
+                uint32_t af[4];
+                ldsm_x4(af, kbase + ks * 32);
+                mma16816(dl, af, qf[ks][0], qf[ks][1]);
+                const float2 ca = *reinterpret_cast<const float2*>(&wb.c[16 * ks + 2 * t4]);
+                const float2 cb = *reinterpret_cast<const float2*>(&wb.c[16 * ks + 2 * t4 + 8]);
+                uint32_t xf[4];
+                xf[0] = xbar_pair(af[0], ca.x, ca.y);
+                xf[1] = xbar_pair(af[1], ca.x, ca.y);
+                xf[2] = xbar_pair(af[2], cb.x, cb.y);
+                xf[3] = xbar_pair(af[3], cb.x, cb.y);
+                mma16816(dx, xf, qf[ks][0], qf[ks][1]);
+            }
+        }
+        // (2) items (row, head): ra = g4 (dl[0], dl[1]), rb = g4 + 8 (dl[2], dl[3]); heads h0, h1
+        const uint32_t ba = wb.bits[st][g4], bb = wb.bits[st][g4 + 8];
+        const float xna = wb.xn[st][g4], xnb = wb.xn[st][g4 + 8];
+        const uint32_t bt[4] = {ba, ba, bb, bb};
+        const int hh[4] = {h0, h1, h0, h1};
+        bool need[4];
+        float cs[4];
+        {
+            const float qn[4] = {qn0, qn1, qn0, qn1};
+            const float xn[4] = {xna, xna, xnb, xnb};
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                need[i] = hh[i] < G && !(bt[i] & 0x100u) && ((bt[i] >> hh[i]) & 1u);
+                const float den = qn[i] * xn[i];
+                const float c = den > 0.0f ? __fdividef(dx[i], den) : 0.0f;
+                cs[i] = fminf(1.0f, fmaxf(-1.0f, c));
+            }
+        }
+        // ln u of the items that need it, compacted over the warp (one MUFU chain per lane per round)
+        float lu[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        {
+            int base = 0, pos[4];
+            const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, need[i]);
+                pos[i] = base + __popc(bal & lt);
+                base += __popc(bal);
+                if (need[i]) wb.items[pos[i]] = cs[i];
+            }
+            __syncwarp();
+            for (int e = lane; e < base; e += 32) {
+                const float p = 1.0f - acosf(wb.items[e]) * 0.3183098861837907f;
+                wb.items[e] = log_sampling_prob(p, a.K, a.L, a.minc);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                if (need[i]) lu[i] = wb.items[pos[i]];
+        }
+        float z[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const float l = dl[i] * INV_SQRT_D;
+            z[i] = (hh[i] < G && (bt[i] & 0x100u)) ? l : (need[i] ? l - lu[i] : -INFINITY);
+        }
+        if (a.weighted) {
+            const int64_t b = cur_u / a.Hkv, hkv = cur_u % a.Hkv, qh0 = b * a.Hq + hkv * G;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int r = (i >> 1) ? g4 + 8 : g4;
+                if (z[i] != -INFINITY && r < nr) {
+                    const int key = wb.key[st][r];
+                    atomicOr(a.weighted + (qh0 + hh[i]) * nwb + (key >> 5), 1u << (key & 31));
+                }
+            }
+        }
+        // (3) online softmax per head (rows of head h are spread over the 8 lanes with the same t4)
+        float mx0 = fmaxf(z[0], z[2]), mx1 = fmaxf(z[1], z[3]);
+#pragma unroll
+        for (int m = 4; m <= 16; m <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, m));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, m));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const bool moved = __any_sync(0xffffffffu, mn0 != m0 || mn1 != m1);
+        const float al0 = m0 == -INFINITY ? 0.0f : __expf(m0 - mn0);
+        const float al1 = m1 == -INFINITY ? 0.0f : __expf(m1 - mn1);
+        const float mnn[4] = {mn0, mn1, mn0, mn1};
+        __nv_bfloat16 whi[4], wlo[4];
+        float wsum0 = 0.0f, wsum1 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const float w = z[i] == -INFINITY ? 0.0f : __expf(z[i] - mnn[i]);
+            whi[i] = __float2bfloat16_rn(w);
+            wlo[i] = __float2bfloat16_rn(w - __bfloat162float(whi[i]));
+            const float we = __bfloat162float(whi[i]) + __bfloat162float(wlo[i]);
+            if (i & 1) wsum1 += we;
+            else wsum0 += we;
+        }
+#pragma unroll
+        for (int m = 4; m <= 16; m <<= 1) {
+            wsum0 += __shfl_xor_sync(0xffffffffu, wsum0, m);
+            wsum1 += __shfl_xor_sync(0xffffffffu, wsum1, m);
+        }
+        s0 = s0 * al0 + wsum0;
+        s1 = s1 * al1 + wsum1;
+        m0 = mn0;
+        m1 = mn1;
+        // weights -> PV B operand [n][row]: hi in column h, lo in column G + h
+        {
+            __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wb.wt);
+            const int rows[4] = {g4, g4, g4 + 8, g4 + 8};
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                if (hh[i] < G) {
+                    wt[hh[i] * SR + rows[i]] = whi[i];
+                    wt[(G + hh[i]) * SR + rows[i]] = wlo[i];
+                }
+            }
+        }
+        __syncwarp();
+        // (4) rescale the running a (per PV column: the head's alpha from the lane that holds it)
+        if (moved) {
+#pragma unroll
+            for (int nt = 0; nt < NT; nt++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const int h = pv_head(nt, i);
+                    const int src = (lane & ~3) | ((h < 0 ? 0 : h) >> 1);
+                    const float x0 = __shfl_sync(0xffffffffu, al0, src);
+                    const float x1 = __shfl_sync(0xffffffffu, al1, src);
+                    const float al = h < 0 ? 0.0f : ((h & 1) ? x1 : x0);
+#pragma unroll
+                    for (int dt = 0; dt < 8; dt++) {
+                        acc[dt][nt][i] *= al;
+                        acc[dt][nt][2 + i] *= al;
+                    }
+                }
+        }
+        // (5) a[d][n] += V^T[d][rows] W[rows][n] on tensor cores (V^T fragments by ldmatrix.trans)
+        {
+            uint32_t bw[NT][2];
+            const uint32_t* wt32 = reinterpret_cast<const uint32_t*>(wb.wt);
+#pragma unroll
+            for (int nt = 0; nt < NT; nt++) {
+                bw[nt][0] = wt32[((nt * 8 + g4) * SR + 2 * t4) >> 1];
+                bw[nt][1] = wt32[((nt * 8 + g4) * SR + 2 * t4 + 8) >> 1];
+            }
+            const int mi = lane >> 3, rr = lane & 7;
+            const int row = (mi >> 1) * 8 + rr;
+            const uint32_t vbase = smem_u32(Vt + row * RP + (mi & 1) * 16);
+#pragma unroll
+            for (int dt = 0; dt < 8; dt++) {
+                uint32_t af[4];
+                ldsm_x4_t(af, vbase + dt * 32);
+#pragma unroll
+                for (int nt = 0; nt < NT; nt++) mma16816(acc[dt][nt], af, bw[nt][0], bw[nt][1]);
+            }
+        }
+        __syncwarp();  // stage buffer, weight tile and items free
+        computed++;
+        issue();  // refill the stage just consumed
+    }
+    if (cur_u >= 0) flush(cur_u);
+}
+
+}  // namespace v7
+
+// ---- host
+static size_t al128e(size_t x) { return (x + 127) & ~(size_t)127; }
+
+size_t estimate_layout(EstArgs& a, int G) {
+    (void)G;
+    const size_t units = (size_t)(a.B * a.Hkv);
+    a.off_wbuf = (int)al128e((units + 1) * 8);
+    return a.off_wbuf + sizeof(v7::WBuf) * v7::NW;
+}
+
+template <int G>
+static int launch_select_g(const EstArgs& a, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.B * a.Hkv));
+    cfg.blockDim = dim3(v7::SEL_WARPS * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, v7::select_kernel<G>, a);
+    count_launch(1);
+    return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_select(const EstArgs& a, cudaStream_t st) {
+    switch ((int)(a.Hq / a.Hkv)) {
+        case 1: return launch_select_g<1>(a, st);
+        case 2: return launch_select_g<2>(a, st);
+        case 4: return launch_select_g<4>(a, st);
+        case 8: return launch_select_g<8>(a, st);
+    }
+    return MAGICPIG_EINVAL;
+}
+
+template <int G>
+static int launch_estimate_g(EstArgs a, int nsm, int max_smem, cudaStream_t st) {
+    const size_t smem = estimate_layout(a, G);
+    if (smem > (size_t)max_smem) return MAGICPIG_EINVAL;
+    auto kern = v7::estimate_kernel<G>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return MAGICPIG_ECUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nsm);
+    cfg.blockDim = dim3(v7::NW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+    count_launch(1);
+    return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_estimate(const EstArgs& a, int nsm, int max_smem, cudaStream_t st) {
+    if (a.B * a.Hkv > EST_MAX_UNITS || a.n_local >= (1 << 24)) return MAGICPIG_EINVAL;
+    switch ((int)(a.Hq / a.Hkv)) {
+        case 1: return launch_estimate_g<1>(a, nsm, max_smem, st);
+        case 2: return launch_estimate_g<2>(a, nsm, max_smem, st);
+        case 4: return launch_estimate_g<4>(a, nsm, max_smem, st);
+        case 8: return launch_estimate_g<8>(a, nsm, max_smem, st);
+    }
+    return MAGICPIG_EINVAL;
+}
+
+}  // namespace mp

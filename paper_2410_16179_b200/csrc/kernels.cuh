@@ -118,4 +118,34 @@ struct AttendArgs {
 size_t attend_layout(AttendArgs& a, int G);
 int launch_attend(const AttendArgs& a, int nsm, int max_smem, cudaStream_t st);
 
+// ---- decode v7: Query (scan6 | bucket_mark) -> S bitmaps -> select (ordered S_g u ... lists per unit)
+//      -> estimate (every warp a contiguous range of the concatenated lists)
+struct EstArgs {
+    const uint16_t* q;
+    const float* center;
+    const float* key_norm;
+    const uint16_t* k;
+    const uint16_t* v;
+    const uint32_t* sbits;        // [B][Hq][ceil(n/32)] S bitmaps of the Query step
+    int64_t B, Hkv, Hq, n_local, seq_offset, n_global, nchunks;
+    int K, L, minc, sink, local;
+    int off_wbuf;                 // set by estimate_layout
+    uint32_t* ents;               // [units][n_local] key | head bits << 24 (union_g S_g, ascending)
+    int32_t* ucnt;                // [units] entries of the unit (D only)
+    int32_t* hcnt;                // [B*Hq] |S_g|
+    uint32_t* s_mask;             // debug: S_g restricted to D
+    uint32_t* weighted;           // debug: (head, key) pairs that received a finite weight
+    float* out;
+    float* partial;
+    int32_t* s_count;
+    uint32_t* unit_ctr;
+    float* parts;
+    uint32_t* status;
+};
+constexpr int EST_WARPS = 8;      // warps per estimator CTA
+constexpr int EST_MAX_UNITS = 4096;
+int launch_select(const EstArgs& a, cudaStream_t st);
+size_t estimate_layout(EstArgs& a, int G);
+int launch_estimate(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
+
 }  // namespace mp

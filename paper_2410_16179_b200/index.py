@@ -125,9 +125,36 @@ class MagicPIG:
         return self
 
     # ------------------------------------------------------------ decode
+    def _check_decode_args(self, q, k, v, out=None, partial=None, s_count=None, s_mask=None):
+        """Shapes and dtypes against the built index: a mismatch would be an out-of-bounds device access."""
+        if self.buf is None:
+            raise B_.MagicPIGError("build the index first")
+        if k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+            raise B_.MagicPIGError("k and v must be bfloat16")
+        if k.dim() != 4 or tuple(k.shape[:3]) != tuple(self.shape) or k.shape[3] != 128 or v.shape != k.shape:
+            raise B_.MagicPIGError(f"k, v must be [B][Hkv][n][128] = {tuple(self.shape)} + (128,) (the built index); "
+                                   f"got {tuple(k.shape)}, {tuple(v.shape)}")
+        Bn, Hkv, n = self.shape
+        if q.dim() != 3 or q.shape[0] != Bn or q.shape[2] != 128 or q.shape[1] % Hkv:
+            raise B_.MagicPIGError(f"q must be [B={Bn}][G*{Hkv}][128]; got {tuple(q.shape)}")
+        if not q.is_cuda and q.dtype == torch.bfloat16:
+            return
+        if q.dtype != torch.bfloat16:
+            raise B_.MagicPIGError("q must be bfloat16")
+        Hq = q.shape[1]
+        if out is not None and (out.dtype != torch.float32 or tuple(out.shape) != (Bn, Hq, 128)):
+            raise B_.MagicPIGError(f"out must be float32 [{Bn}][{Hq}][128]")
+        if partial is not None and (partial.dtype != torch.float32 or partial.numel() != Bn * Hq * B_.PART):
+            raise B_.MagicPIGError(f"partial must be float32 [{Bn * Hq}][{B_.PART}]")
+        if s_count is not None and (s_count.dtype != torch.int32 or s_count.numel() != Bn * Hq):
+            raise B_.MagicPIGError(f"s_count must be int32 [{Bn}][{Hq}]")
+        if s_mask is not None and (s_mask.dtype != torch.int32 or s_mask.numel() != Bn * Hq * ((n + 31) // 32)):
+            raise B_.MagicPIGError(f"s_mask must be int32 [{Bn}][{Hq}][{(n + 31) // 32}]")
+
     def decode(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out=None, partial=None,
                s_count=None, s_mask=None):
         """One decode step for q [B][Hq][128] bf16 over this rank's keys."""
+        self._check_decode_args(q, k, v, out, partial, s_count, s_mask)
         Bn, Hkv, n, _ = k.shape
         Hq = q.shape[1]
         ws = self.decode_workspace(Bn, Hq, Hkv, n, q.device)
@@ -141,6 +168,23 @@ class MagicPIG:
             B_.decode(self.cfg, q, b.codes, b.center, b.key_norm, k, v, self.seq_offset, self.n_global, self.W, ws,
                       out=out, partial=partial, s_count=s_count, s_mask=s_mask)
         return out if out is not None else partial
+
+    def decode_host(self, q_host: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out_host=None):
+        """One serving step from host memory through the C ABI (magicpig_decode_host): q_host [B][Hq][128]
+        bf16 on the CPU (pinned for an asynchronous copy) -> out_host [B][Hq][128] float32 on the CPU,
+        valid on return.  Unsharded indexes only."""
+        self._check_decode_args(q_host, k, v)
+        if self.seq_offset != 0 or self.n_global != self.shape[2]:
+            raise B_.MagicPIGError("decode_host is for unsharded indexes")
+        Bn, Hkv, n, _ = k.shape
+        Hq = q_host.shape[1]
+        if out_host is None:
+            out_host = torch.empty((Bn, Hq, 128), dtype=torch.float32).pin_memory()
+        ws = self.decode_workspace(Bn, Hq, Hkv, n, k.device)
+        b = self.buf
+        B_.decode_host(self.cfg, q_host, None if self.buckets else b.codes, b.tables if self.buckets else None,
+                       b.center, b.key_norm, k, v, self.W, out_host, ws)
+        return out_host
 
     def decode_sharded(self, q, k_local, v_local, group=None, out=None, s_count=None):
         """Sequence-sharded decode: partial states, one all-gather, fixed-order merge."""
@@ -175,6 +219,9 @@ class DecodeSession:
         self.out_dev = torch.zeros((Bn, Hq, 128), dtype=torch.float32, device=dev)
         mp.decode_workspace(Bn, Hq, Hkv, n, dev)
         self._mp, self._k, self._v = mp, k, v
+        # the graph holds raw pointers: keep every buffer it captured alive, and refuse to replay
+        # once the index was rebuilt or the workspace replaced
+        self._held = (mp.buf, mp._ws_dec, mp.W)
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):  # warm-up outside the capture (library attributes, allocations)
@@ -192,6 +239,9 @@ class DecodeSession:
         self.out_host.copy_(self.out_dev, non_blocking=True)
 
     def step(self):
+        if self._mp.buf is not self._held[0] or self._mp._ws_dec is not self._held[1]:
+            raise B_.MagicPIGError("the index or its workspace changed since this session was captured; "
+                                   "create a new session")
         self.graph.replay()
         return self.out_host
 

@@ -20,18 +20,19 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-3
 
 
-@pytest.fixture(params=[6, 5], ids=["k6", "k5"], autouse=True)
+@pytest.fixture(params=[7, 6, 5], ids=["k7", "k6", "k5"], autouse=True)
 def decode_kernel(request):
-    """Every parity test runs on two decode paths: 6 = Query kernel + estimator kernel (the
-    default) and 5 = the persistent fused kernel (which falls back to the cluster-per-chunk
-    kernel 4 when its shared memory does not fit); they must agree with the oracle
-    independently."""
+    """Every parity test runs on three decode paths: 7 = Query kernel + select kernel (ordered
+    S_g u T lists) + balanced estimator kernel (the default), 6 = Query kernel + estimator kernel
+    with a producer warp, and 5 = the persistent fused kernel (which falls back to the
+    cluster-per-chunk kernel 4 when its shared memory does not fit); they must agree with the
+    oracle independently."""
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device (no fallback)")
     pkg = _pkg()
     pkg.binding.set_decode_kernel(request.param)
     yield request.param
-    pkg.binding.set_decode_kernel(6)
+    pkg.binding.set_decode_kernel(7)
 
 
 def _dev():
@@ -367,8 +368,8 @@ def test_weighted_set_is_s_union_t(G, buckets, decode_kernel):
     """The compacted list the estimator gathers, exported as the (head, key) pairs that received a
     finite weight: it must equal S_g u T exactly (oracle), and S_g restricted to D must equal the
     oracle's S_g (Alg. 1)."""
-    if decode_kernel != 6:
-        pytest.skip("weighted-set export exists on the v6 path")
+    if decode_kernel < 6:
+        pytest.skip("weighted-set export exists on the v6 / v7 paths")
     pkg = _pkg()
     n = 5000
     wl = synth.Workload("wset", 960 + G + 10 * buckets, B=2, Hq=2 * G, Hkv=2, n=n, K=8, L=40, sink=4, local=64)

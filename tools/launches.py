@@ -25,4 +25,4 @@ for fn in sys.argv[1:]:
         t = sum(m.get("gpu__time_duration.sum", 0) for m in ms) / len(ms) / 1e3
         rd = sum(m.get("dram__bytes_read.sum", 0) for m in ms) / len(ms) / 1e6
         wr = sum(m.get("dram__bytes_write.sum", 0) for m in ms) / len(ms) / 1e6
-        print(f"  {k:60s} n={len(ms):3d} {t:9.2f} us  read {rd:8.2f} MB  write {wr:6.2f} MB  {rd / max(t, 1e-9) / 1e3:6.2f} TB/s")
+        print(f"  {k:60s} n={len(ms):3d} {t:9.2f} us  read {rd:8.2f} MB  write {wr:6.2f} MB  {(rd + wr) / max(t, 1e-9):6.2f} TB/s")

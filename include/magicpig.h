@@ -264,6 +264,20 @@ int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, const uint16_
                                        unsigned long long* timeline, int64_t timeline_len, void* ws,
                                        size_t ws_bytes, void* stream);
 
+/* The same timeline over the bucketed tables.  With decode kernel 7 (the default)
+ * both calls write per-WARP stamps of the estimator kernel, timeline[row][16]
+ * (row = cta * 8 + warp; ns since epoch, 0 = not reached): 0 start, 1 after
+ * griddepcontrol.wait, 2 unit prefix done, 3 first entries loaded, 4 first
+ * slabs issued, 5 first slab's rows arrived, 6 last slab computed, 7 flush
+ * start, 8 unit merge start, 9 unit merge end, 10 end; 11 slabs computed,
+ * 12 unit merges done; and return the number of rows. */
+int64_t magicpig_debug_decode_timeline_buckets(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                               const int32_t* tables, const float* center, const float* key_norm,
+                                               const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
+                                               int64_t n_local, const float* W, float* out,
+                                               unsigned long long* timeline, int64_t timeline_len, void* ws,
+                                               size_t ws_bytes, void* stream);
+
 /* Debug: one decode step (encode + Query + estimator) that also exports the sets
  * the estimator actually used:
  *   s_mask[B][Hq][ceil(n_local/32)]    S_g restricted to D (the Query result), or NULL

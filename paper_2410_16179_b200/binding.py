@@ -74,6 +74,8 @@ _SIGS = {
     "magicpig_debug_decode_stage": ([_p, _i, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _sz, _p],
                                     _i),
     "magicpig_debug_build_phases": ([_p, _p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p, _p], _i),
+    "magicpig_debug_decode_timeline_buckets": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p,
+                                                _i64, _p, _sz, _p], _i64),
     "magicpig_strerror": ([_i], C.c_char_p),
     "magicpig_version": ([], C.c_char_p),
     "magicpig_launch_count": ([], C.c_uint64),
@@ -301,8 +303,18 @@ def debug_hash_acc(cfg, k_unit, W, center, r2, acc, ws):
                                          _ptr(ws), ws.numel(), _stream()), "debug_hash_acc")
 
 
-def debug_decode_timeline(cfg, q, codes, center, key_norm, k, v, W, out, timeline, ws) -> int:
+def debug_decode_timeline(cfg, q, codes, center, key_norm, k, v, W, out, timeline, ws, buckets=False) -> int:
+    """Kernel 5: per-CTA stamps [grid][32]; kernel 7: per-warp stamps [rows][16] (returns rows).  With
+    buckets=True, `codes` is the bucketed tables."""
     Bn, Hkv, n, _ = k.shape
+    if buckets:
+        rc = lib().magicpig_debug_decode_timeline_buckets(_cfg(cfg), _ptr(q), q.shape[1], _ptr(codes), _ptr(center),
+                                                          _ptr(key_norm), _ptr(k), _ptr(v), Bn, Hkv, n, _ptr(W),
+                                                          _ptr(out), _ptr(timeline), timeline.numel(), _ptr(ws),
+                                                          ws.numel(), _stream())
+        if rc < 0:
+            _check(int(rc), "debug_decode_timeline")
+        return int(rc)
     Hq = q.shape[1]
     rc = lib().magicpig_debug_decode_timeline(_cfg(cfg), _ptr(q), Hq, _ptr(codes), _ptr(center), _ptr(key_norm),
                                               _ptr(k), _ptr(v), Bn, Hkv, n, _ptr(W), _ptr(out), _ptr(timeline),

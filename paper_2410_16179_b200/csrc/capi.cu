@@ -121,14 +121,16 @@ static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, in
 
 struct DecodeWs {
     uint32_t* status;
+    float* lutab;
     uint32_t* qbits;
     uint32_t* unit_ctr;
     float* parts;
     int32_t* chunk_cnt;
     uint32_t* sbits;
     uint32_t* ents;
-    int32_t* ucnt;
-    int32_t* hcnt;
+    int32_t* pcnt;
+    int32_t* hpc;
+    int2* urec;
     uint16_t* qstage;  // magicpig_decode_host: q copied from the host
     float* ostage;     //                       out before the copy to the host
     size_t bytes;
@@ -150,6 +152,7 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
         return r;
     };
     w.status = (uint32_t*)take(256);
+    w.lutab = (float*)take((size_t)LUT_WORDS * 4);
     w.qbits = (uint32_t*)take((size_t)B * Hq * g.KLw * 4);
     w.unit_ctr = (uint32_t*)take((size_t)units * 4);
     const int64_t nT = n_local < (int64_t)c->sink + c->local ? n_local : (int64_t)c->sink + c->local;
@@ -159,9 +162,10 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     w.parts = (float*)take(parts4 > parts5 ? parts4 : parts5);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
     w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4);  // S bitmaps of the Query step
-    w.ents = (uint32_t*)take((size_t)units * (n_local > 0 ? n_local : 1) * 4);  // v7 unit lists
-    w.ucnt = (int32_t*)take((size_t)units * 4);
-    w.hcnt = (int32_t*)take((size_t)B * Hq * 4);
+    w.ents = (uint32_t*)take((size_t)units * nch * KCHUNK * 4);  // v7 piece lists
+    w.pcnt = (int32_t*)take((size_t)units * nch * 4);
+    w.hpc = (int32_t*)take((size_t)B * Hq * nch * 4);
+    w.urec = (int2*)take((size_t)units * 8);
     w.qstage = (uint16_t*)take((size_t)B * Hq * HD * 2);
     w.ostage = (float*)take((size_t)B * Hq * HD * 4);
     w.bytes = off;
@@ -272,7 +276,8 @@ int magicpig_encode_queries(const magicpig_config* cfg, const uint16_t* q, int64
     DecodeWs w = decode_layout(cfg, B, Hq, 1, 0, ws);
     const Geom g = make_geom(cfg->K, cfg->L, 0);
     if (ws_bytes < (size_t)((uint8_t*)w.qbits - (uint8_t*)ws) + (size_t)B * Hq * g.KLw * 4) return MAGICPIG_EWORKSPACE;
-    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream));
+    return launch_qencode(q, B * Hq, W, g.KL, g.KLw, w.qbits, w.status, S(stream), cfg->K, cfg->L,
+                          cfg->min_collisions, w.lutab);
 }
 
 static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq, const uint32_t* codes,
@@ -357,7 +362,19 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
     const int kver = g_decode_kernel.load();
-    if ((kver % 10 == 6 || kver % 10 == 7) && !timeline) {
+    if ((kver % 10 == 6 && !timeline) || kver % 10 == 7) {
+        const bool v7 = kver % 10 == 7 && B * Hkv * (g.nchunks + 1) <= EST_MAX_PIECES && n_local < (1 << 24);
+        EstArgs ea;
+        memset(&ea, 0, sizeof(ea));
+        ea.q = q, ea.center = center, ea.key_norm = key_norm, ea.k = k, ea.v = v, ea.sbits = w.sbits;
+        ea.B = B, ea.Hkv = Hkv, ea.Hq = Hq, ea.n_local = n_local, ea.seq_offset = seq_offset;
+        ea.n_global = n_global, ea.nchunks = g.nchunks;
+        ea.K = cfg->K, ea.L = cfg->L, ea.minc = cfg->min_collisions, ea.sink = cfg->sink, ea.local = cfg->local;
+        ea.ents = w.ents, ea.pcnt = w.pcnt, ea.hpc = w.hpc, ea.s_mask = s_mask, ea.weighted = weighted;
+        ea.out = out, ea.partial = partial, ea.s_count = s_count;
+        ea.unit_ctr = w.unit_ctr, ea.parts = w.parts, ea.status = w.status, ea.urec = w.urec;
+        ea.lutab = w.lutab;
+        const bool fused = v7 && !tables;  // the dense scan emits the piece lists itself
         // Query(HT, q_code) -> S bitmaps: bucketed tables or the dense code scan (PDL after the encode)
         int rc = 0;
         if (!(stages & 1)) {
@@ -374,24 +391,23 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
             sa.tiles = B * Hkv * g.nchunks;
             sa.K = cfg->K, sa.L = cfg->L, sa.KL = g.KL, sa.KLw = g.KLw, sa.KLq = g.KLq, sa.ngroups = g.ngroups;
             sa.minc = cfg->min_collisions;
+            if (fused) sa.fuse = 1, sa.est = ea;
             rc = launch_scan6(sa, num_sms(), max_smem_optin(), st);
         }
         if (rc || !(stages & 6)) return rc;
-        if (kver % 10 == 7 && B * Hkv <= EST_MAX_UNITS && n_local < (1 << 24)) {
-            // ordered S_g u ... lists per unit, then the balanced estimator
-            EstArgs ea;
-            memset(&ea, 0, sizeof(ea));
-            ea.q = q, ea.center = center, ea.key_norm = key_norm, ea.k = k, ea.v = v, ea.sbits = w.sbits;
-            ea.B = B, ea.Hkv = Hkv, ea.Hq = Hq, ea.n_local = n_local, ea.seq_offset = seq_offset;
-            ea.n_global = n_global, ea.nchunks = g.nchunks;
-            ea.K = cfg->K, ea.L = cfg->L, ea.minc = cfg->min_collisions, ea.sink = cfg->sink, ea.local = cfg->local;
-            ea.ents = w.ents, ea.ucnt = w.ucnt, ea.hcnt = w.hcnt, ea.s_mask = s_mask, ea.weighted = weighted;
-            ea.out = out, ea.partial = partial, ea.s_count = s_count;
-            ea.unit_ctr = w.unit_ctr, ea.parts = w.parts, ea.status = w.status;
-            if (grid_out) *grid_out = num_sms();
-            if (stages & 2) rc = launch_select(ea, st);
+        if (v7) {
+            // ordered S_g u ... lists per unit, then the balanced estimator and the unit merge
+            if (grid_out) *grid_out = (int64_t)num_sms() * EST_WARPS;  // timeline rows (one per warp)
+            if (timeline) {
+                const size_t rows = (size_t)num_sms() * EST_WARPS;
+                if (timeline_len < (int64_t)rows * 16) return MAGICPIG_EINVAL;
+                if (cudaMemsetAsync(timeline, 0, rows * 16 * 8, st) != cudaSuccess) return MAGICPIG_ECUDA;
+                ea.timeline = timeline;
+            }
+            if ((stages & 2) && !fused) rc = launch_select(ea, st);
             if (rc || !(stages & 4)) return rc;
-            return launch_estimate(ea, num_sms(), max_smem_optin(), st);
+            rc = launch_estimate(ea, num_sms(), max_smem_optin(), st);
+            return rc ? rc : launch_est_merge(ea, st);
         }
         // estimator over S_g u T
         AttendArgs aa;
@@ -458,6 +474,22 @@ extern "C" int64_t magicpig_debug_decode_timeline(const magicpig_config* cfg, co
     int64_t grid = 0;
     rc = decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, 0, n_local, out, nullptr, nullptr,
                      nullptr, ws, ws_bytes, stream, timeline, timeline_len, &grid);
+    return rc ? rc : grid;
+}
+
+extern "C" int64_t magicpig_debug_decode_timeline_buckets(const magicpig_config* cfg, const uint16_t* q, int64_t Hq,
+                                                          const int32_t* tables, const float* center,
+                                                          const float* key_norm, const uint16_t* k, const uint16_t* v,
+                                                          int64_t B, int64_t Hkv, int64_t n_local, const float* W,
+                                                          float* out, unsigned long long* timeline,
+                                                          int64_t timeline_len, void* ws, size_t ws_bytes,
+                                                          void* stream) {
+    if (!timeline || !tables || !buckets_ok(cfg, n_local)) return MAGICPIG_EINVAL;
+    int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
+    if (rc) return rc;
+    int64_t grid = 0;
+    rc = decode_impl(cfg, q, Hq, nullptr, center, key_norm, k, v, B, Hkv, n_local, 0, n_local, out, nullptr, nullptr,
+                     nullptr, ws, ws_bytes, stream, timeline, timeline_len, &grid, tables);
     return rc ? rc : grid;
 }
 

@@ -34,12 +34,11 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "pieces.cuh"
 
 namespace mp {
 namespace v7 {
 
-constexpr int SEL_WARPS = 16;  // select CTA
-constexpr int CPW = 4;         // chunks per select warp per round
 constexpr int NW = EST_WARPS;  // estimator warps per CTA
 constexpr int SR = 16;         // rows per slab (mma M)
 constexpr int NST = 2;         // row stages per warp
@@ -53,7 +52,7 @@ struct __align__(128) WBuf {
     uint8_t k[NST][SR * RP];  // K rows
     uint8_t v[NST][SR * RP];  // V rows
     float xn[NST][SR];        // |xbar_i|
-    float c[HD];              // centering vector of the warp's current unit (16-B aligned: float4 stores)
+    float c[HD];              // -c: negated centering vector of the warp's current unit (16-B aligned)
     float items[SR * 8];      // compacted (row, head) items: cos in, ln u out
     uint16_t wt[16 * SR];     // PV B operand: [column n][row] bf16 (hi | lo weights)
     int key[NST][SR];         // local key index of each row
@@ -90,147 +89,42 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// bf16 pair (lo = element c, hi = element c+1) -> bf16(fl32(k - c)) pair (cvt.rn.bf16x2)
-__device__ __forceinline__ uint32_t xbar_pair(uint32_t kw, float c0, float c1) {
-    const __nv_bfloat162 xb = __floats2bfloat162_rn(__fsub_rn(__uint_as_float(kw << 16), c0),
-                                                    __fsub_rn(__uint_as_float(kw & 0xffff0000u), c1));
+// bf16 pair (lo = element d, hi = element d+1) -> bf16(fl32(k - c)) pair: one packed fp32 add (FADD2) of
+// the negated centering vector, one cvt.rn.bf16x2
+__device__ __forceinline__ uint32_t xbar_pair(uint32_t kw, float2 nc) {
+    const float2 x = __fadd2_rn(make_float2(__uint_as_float(kw << 16), __uint_as_float(kw & 0xffff0000u)), nc);
+    const __nv_bfloat162 xb = __floats2bfloat162_rn(x.x, x.y);
     return *reinterpret_cast<const uint32_t*>(&xb);
 }
-__device__ __forceinline__ uint32_t range_mask(int64_t base, int64_t lo, int64_t hi) {
-    int64_t x = lo - base, y = hi - base;
-    x = x < 0 ? 0 : (x > 32 ? 32 : x);
-    y = y < 0 ? 0 : (y > 32 ? 32 : y);
-    if (y <= x) return 0u;
-    const uint32_t hiMask = y >= 32 ? 0xffffffffu : ((1u << y) - 1u);
-    const uint32_t loMask = x >= 32 ? 0xffffffffu : ((1u << x) - 1u);
-    return hiMask & ~loMask;
-}
-__device__ __forceinline__ float warp_sum_f(float v) {
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-    return v;
-}
-__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
-#pragma unroll
-    for (int m = 1; m < 32; m <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, v, m);
-        if (lane >= m) v += x;
-    }
-    return v;
-}
-
-// static keys T on this shard (sink tokens at global [0, sink), local window at [n - local, n)),
-// as local index ranges [lo1, lo1 + len1) u [lo2, lo2 + len2)
-struct StaticRanges {
-    int64_t lo1, len1, lo2, len2;
-};
-__device__ __forceinline__ StaticRanges static_ranges(const EstArgs& a) {
-    StaticRanges r;
-    const int64_t off = a.seq_offset, nl = a.n_local;
-    r.lo1 = max((int64_t)0, -off);
-    const int64_t hi1 = min(nl, (int64_t)a.sink - off);
-    r.len1 = hi1 > r.lo1 ? hi1 - r.lo1 : 0;
-    r.lo2 = max((int64_t)0, a.n_global - a.local - off);
-    const int64_t hi2 = min(nl, a.n_global - off);
-    if (r.len1 > 0 && r.lo2 < hi1) r.lo2 = hi1;
-    r.len2 = hi2 > r.lo2 ? hi2 - r.lo2 : 0;
-    return r;
-}
-
 // ============================================================================ select
+// One warp per piece = (unit, 1024-key chunk): S_g restricted to D for the unit's G heads (lane = 32-key
+// word), the union compacted in ascending key order into the piece's list (capacity 1024), the list
+// length and |S_g| of the piece.  Pieces are independent (no cross-chunk order is needed: the estimator
+// concatenates them through a prefix over the piece lengths).
+constexpr int SEL_WPB = 8;  // warps (pieces) per CTA
+
 template <int G>
-__global__ void __launch_bounds__(SEL_WARPS * 32) select_kernel(EstArgs a) {
+__global__ void __launch_bounds__(SEL_WPB * 32) select_kernel(EstArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ int wtot[SEL_WARPS];
-    __shared__ int hsum[SEL_WARPS][8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t u = blockIdx.x, b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t pid = (int64_t)blockIdx.x * SEL_WPB + warp;
+    if (pid >= a.B * a.Hkv * a.nchunks) return;
+    const int64_t u = pid / a.nchunks, c = pid % a.nchunks;
+    const int64_t b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
     const int64_t nwb = (a.n_local + 31) >> 5;
     const StaticRanges sr = static_ranges(a);
-    uint32_t* ents = a.ents + u * a.n_local;
-    int hc[G];
-#pragma unroll
-    for (int g = 0; g < G; g++) hc[g] = 0;
-    int64_t run = 0;
+    const int64_t wi = c * 32 + lane;
+    const bool ok = wi < nwb;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // S bitmaps of the Query kernel
-#pragma unroll 1
-    for (int64_t r0 = 0; r0 < a.nchunks; r0 += SEL_WARPS * CPW) {
-        uint32_t sg[CPW][G];
+    uint32_t sg[G];
 #pragma unroll
-        for (int j = 0; j < CPW; j++) {
-            const int64_t wi = (r0 + warp * CPW + j) * 32 + lane;
-            const bool ok = r0 + warp * CPW + j < a.nchunks && wi < nwb;
-#pragma unroll
-            for (int g = 0; g < G; g++) sg[j][g] = ok ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
-        }
-        int cex[CPW], ctot[CPW], wt = 0;
-#pragma unroll
-        for (int j = 0; j < CPW; j++) {
-            const int64_t wi = (r0 + warp * CPW + j) * 32 + lane;
-            const int64_t base = wi * 32;
-            const uint32_t dmask = range_mask(base, 0, a.n_local) &
-                                   ~(range_mask(base, sr.lo1, sr.lo1 + sr.len1) |
-                                     range_mask(base, sr.lo2, sr.lo2 + sr.len2));
-            uint32_t un = 0u;
-#pragma unroll
-            for (int g = 0; g < G; g++) {
-                sg[j][g] &= dmask;
-                un |= sg[j][g];
-                hc[g] += __popc(sg[j][g]);
-            }
-            if (a.s_mask && r0 + warp * CPW + j < a.nchunks && wi < nwb) {
-#pragma unroll
-                for (int g = 0; g < G; g++) a.s_mask[(qh0 + g) * nwb + wi] = sg[j][g];
-            }
-            const int c = __popc(un);
-            const int incl = warp_incl_scan(c, lane);
-            cex[j] = wt + incl - c;
-            ctot[j] = __shfl_sync(0xffffffffu, incl, 31);
-            wt += ctot[j];
-        }
-        if (lane == 0) wtot[warp] = wt;
-        __syncthreads();
-        int woff = 0, rtot = 0;
-#pragma unroll
-        for (int w = 0; w < SEL_WARPS; w++) {
-            const int x = wtot[w];
-            woff += w < warp ? x : 0;
-            rtot += x;
-        }
-#pragma unroll
-        for (int j = 0; j < CPW; j++) {
-            const int64_t base = ((r0 + warp * CPW + j) * 32 + lane) * 32;
-            uint32_t un = 0u;
-#pragma unroll
-            for (int g = 0; g < G; g++) un |= sg[j][g];
-            int64_t pos = run + woff + cex[j];
-            while (un) {
-                const int bit = __ffs(un) - 1;
-                un &= un - 1u;
-                uint32_t hb = 0u;
-#pragma unroll
-                for (int g = 0; g < G; g++) hb |= ((sg[j][g] >> bit) & 1u) << g;
-                ents[pos++] = (uint32_t)(base + bit) | (hb << 24);
-            }
-        }
-        run += rtot;
-        __syncthreads();  // wtot reusable
-    }
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        int c = hc[g];
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
-        if (lane == 0) hsum[warp][g] = c;
-    }
-    __syncthreads();
-    if (tid < G) {
-        int c = 0;
-#pragma unroll
-        for (int w = 0; w < SEL_WARPS; w++) c += hsum[w][tid];
-        a.hcnt[qh0 + tid] = c;
-    }
-    if (tid == 0) a.ucnt[u] = (int32_t)run;
+    for (int g = 0; g < G; g++) sg[g] = ok ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
+    emit_piece<G>(a, sr, u, c, qh0, lane, sg);
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 // ============================================================================ estimate
@@ -241,16 +135,25 @@ template <int G>
 __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
     constexpr int NT = (2 * G + 7) / 8;  // PV n-tiles: columns [hi heads | lo heads | pad]
     extern __shared__ __align__(128) uint8_t dsm[];
-    int64_t* pref = reinterpret_cast<int64_t*>(dsm);  // [units + 1] first entry of each unit
-    __shared__ long long wsum[NW];
+    // pref[p] = first entry of piece p in the concatenation; piece u * P = unit u's static keys, piece
+    // u * P + 1 + c = the list of chunk c of unit u (P = nchunks + 1)
+    int* pref = reinterpret_cast<int*>(dsm);
+    __shared__ int wsum[NW];
     WBuf* wbuf = reinterpret_cast<WBuf*>(dsm + a.off_wbuf);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t units = a.B * a.Hkv;
     const int64_t nwb = (a.n_local + 31) >> 5;
     const StaticRanges sr = static_ranges(a);
-    const int64_t nT = sr.len1 + sr.len2;
+    const int nT = (int)(sr.len1 + sr.len2);
+    const int P = (int)a.nchunks + 1;
+    const int NP = (int)units * P;
     WBuf& wb = wbuf[warp];
+    unsigned long long* tl = a.timeline ? a.timeline + ((size_t)blockIdx.x * NW + warp) * 16 : nullptr;
+    auto stamp = [&](int i) {
+        if (tl && lane == 0) tl[i] = gtimer();
+    };
+    stamp(0);
 
     if (lane < NST) mbar_init(&wb.bar[lane], 33);  // 1 expect_tx + 32 noinc arrivals
     // rows a slab does not load must hold finite values (0 * stale = 0); pad columns of the PV weights stay 0
@@ -259,54 +162,52 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
     for (int e = lane; e < 8 * SR; e += 32) reinterpret_cast<uint32_t*>(wb.wt)[e] = 0u;
     fence_mbar_init();
     fence_proxy_async();
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // lists of the select kernel
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // lists of the select step
+    stamp(1);
 
-    // ---- unit prefix over the concatenated lists: unit u = its static keys, then its list
-    {
-        const int64_t per = (units + NW * 32 - 1) / (NW * 32);
-        const int64_t u0 = min(units, (int64_t)tid * per), u1 = min(units, u0 + per);
-        int64_t s = 0;
-        for (int64_t u = u0; u < u1; u++) s += nT + (int64_t)__ldcg(a.ucnt + u);
-        long long incl = s;
-#pragma unroll
-        for (int m = 1; m < 32; m <<= 1) {
-            const long long x = __shfl_up_sync(0xffffffffu, incl, m);
-            if (lane >= m) incl += x;
+    {   // block exclusive scan of the piece lengths (coalesced loads into smem, then per-thread segments)
+        for (int pp = tid; pp < NP; pp += NW * 32) {
+            const int u = pp / P, cc = pp - u * P;
+            pref[pp] = cc == 0 ? nT : __ldcg(a.pcnt + (int64_t)u * a.nchunks + cc - 1);
         }
+        __syncthreads();
+        const int per = (NP + NW * 32 - 1) / (NW * 32);
+        const int p0 = min(NP, tid * per), p1 = min(NP, p0 + per);
+        int sum = 0;
+        for (int pp = p0; pp < p1; pp++) sum += pref[pp];
+        const int incl = warp_incl_scan(sum, lane);
         if (lane == 31) wsum[warp] = incl;
         __syncthreads();
-        int64_t off = 0;
-        for (int w = 0; w < warp; w++) off += wsum[w];
-        int64_t run = off + incl - s;
-        for (int64_t u = u0; u < u1; u++) {
-            pref[u] = run;
-            run += nT + (int64_t)__ldcg(a.ucnt + u);
+        int run = 0;
+        for (int w = 0; w < warp; w++) run += wsum[w];
+        run += incl - sum;
+        for (int pp = p0; pp < p1; pp++) {
+            const int len = pref[pp];
+            pref[pp] = run;
+            run += len;
         }
-        if (tid == NW * 32 - 1) pref[units] = run;
+        if (tid == NW * 32 - 1) pref[NP] = run;
         __syncthreads();
     }
-    const int64_t E = pref[units];
-    // units with no entry at all (S and T empty): zero output, degenerate status
-    if (blockIdx.x == 0) {
-        for (int64_t u = tid; u < units; u += NW * 32) {
-            if (pref[u + 1] != pref[u]) continue;
-            const int64_t b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
-            for (int g = 0; g < G; g++) {
-                const int64_t row = qh0 + g;
-                for (int d = 0; d < HD; d++) {
-                    if (a.out) a.out[row * HD + d] = 0.0f;
-                    if (a.partial) a.partial[row * PART + 2 + d] = 0.0f;
-                }
-                if (a.partial) a.partial[row * PART] = -INFINITY, a.partial[row * PART + 1] = 0.0f;
-                if (a.s_count) a.s_count[row] = a.hcnt[row];
-            }
-            if (a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
-        }
-    }
-    if (E == 0) return;
+    const int64_t E = pref[NP];
+    stamp(2);
     const int64_t Wt = (int64_t)gridDim.x * NW;
     int64_t Wa = (E + SR * SPW - 1) / (SR * SPW);
     Wa = Wa < 1 ? 1 : (Wa > Wt ? Wt : Wa);
+    // record table for the merge kernel: unit u's records are parts[u + k], k = k_lo .. k_lo + np - 1
+    if (blockIdx.x == 0) {
+        for (int64_t u = tid; u < units; u += NW * 32) {
+            int2 r = make_int2(0, 0);
+            const int64_t e0 = pref[u * P], e1 = pref[(u + 1) * P];
+            if (e1 > e0) {
+                const int64_t k_lo = owner_of(e0, E, Wa), k_hi = owner_of(e1 - 1, E, Wa);
+                r = make_int2((int)k_lo, (int)(k_hi - k_lo + 1));
+            }
+            a.urec[u] = r;
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (E == 0) return;
     const int64_t kw = (int64_t)warp * gridDim.x + blockIdx.x;  // active warps spread over the CTAs first
     if (kw >= Wa) return;
     const int64_t e_lo = kw * E / Wa, e_hi = (kw + 1) * E / Wa;
@@ -319,56 +220,65 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
         const int n = nt * 8 + 2 * t4 + i;
         return n < G ? n : (n < 2 * G ? n - G : -1);
     };
-    auto find_unit = [&](int64_t e) {  // last u with pref[u] <= e (pref nondecreasing, pref[0] = 0)
-        int64_t lo = 0, hi = units;
+    auto find_piece = [&](int64_t e) {  // last piece p with pref[p] <= e (pref nondecreasing, pref[0] = 0)
+        int lo = 0, hi = NP;
         while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
+            const int mid = (lo + hi) >> 1;
             if (pref[mid] <= e) lo = mid;
             else hi = mid;
         }
         return lo;
     };
 
-    // plan: the next slab to issue (unit, first entry, rows) with this lane's entry prefetched
-    int64_t pu = find_unit(e_lo), pcur = e_lo;
-    while (pref[pu + 1] <= pcur) pu++;
-    int p_nr = 0, p_key = 0;
-    uint32_t p_bits = 0u;
-    auto plan = [&]() {
-        if (pcur >= e_hi) {
-            p_nr = 0;
-            return;
-        }
-        while (pref[pu + 1] <= pcur) pu++;
-        const int64_t uend = min(e_hi, pref[pu + 1]);
-        p_nr = (int)min((int64_t)SR, uend - pcur);
+    // plans of the next two slabs to issue (unit, rows, this lane's entry), so the entry loads of a slab
+    // are in flight one whole slab before its row copies are issued
+    struct Plan {
+        int64_t u;
+        int nr, key;
+        uint32_t bits;
+    };
+    int ps = find_piece(e_lo);  // piece holding the plan cursor
+    int64_t pcur = e_lo;
+    auto plan_next = [&](Plan& PL) {
+        PL.nr = 0;
+        PL.key = 0;
+        PL.bits = 0u;
+        if (pcur >= e_hi) return;
+        while (pref[ps + 1] <= pcur) ps++;
+        const int u = ps / P;
+        const int64_t uend = min(e_hi, (int64_t)pref[(u + 1) * P]);
+        PL.u = u;
+        PL.nr = (int)min((int64_t)SR, uend - pcur);
         const int r = lane & 15;
-        p_key = 0;
-        p_bits = 0u;
-        if (r < p_nr) {
-            const int64_t j = pcur - pref[pu] + r;
-            if (j < nT) {
-                p_key = (int)(j < sr.len1 ? sr.lo1 + j : sr.lo2 + (j - sr.len1));
-                p_bits = 0x100u | ((1u << G) - 1u);
+        if (r < PL.nr) {
+            const int e = (int)(pcur + r);
+            int pi = ps;
+            while (pref[pi + 1] <= e) pi++;
+            const int j = e - pref[pi], cc = pi - u * P;
+            if (cc == 0) {
+                PL.key = (int)(j < sr.len1 ? sr.lo1 + j : sr.lo2 + (j - sr.len1));
+                PL.bits = 0x100u | ((1u << G) - 1u);
             } else {
-                const uint32_t e = __ldcg(a.ents + pu * a.n_local + (j - nT));
-                p_key = (int)(e & 0xffffffu);
-                p_bits = e >> 24;
+                const uint32_t ent = __ldcg(a.ents + ((int64_t)u * a.nchunks + cc - 1) * KCHUNK + j);
+                PL.key = (int)(ent & 0xffffffu);
+                PL.bits = ent >> 24;
             }
         }
+        pcur += PL.nr;
     };
+    Plan P0, P1;
     int issued = 0, computed = 0;
     auto issue = [&]() {
-        if (p_nr == 0) return;
+        if (P0.nr == 0) return;
         const int st = issued % NST;
         const int r = lane & 15;
-        const int nr = p_nr;
+        const int nr = P0.nr;
         if (lane < 16) {
-            wb.key[st][r] = p_key;
-            wb.bits[st][r] = p_bits;
+            wb.key[st][r] = P0.key;
+            wb.bits[st][r] = P0.bits;
         }
         if (lane == 0) {
-            wb.su[st] = pu;
+            wb.su[st] = P0.u;
             wb.snr[st] = nr;
         }
         uint64_t* bar = &wb.bar[st];
@@ -376,7 +286,7 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
         if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)nr * 512u);
         __syncwarp();
         if (r < nr) {
-            const int64_t row = pu * a.n_local + p_key;
+            const int64_t row = P0.u * a.n_local + P0.key;
             if (lane < 16) {
                 bulk_g2s(wb.k[st] + r * RP, a.k + row * HD, 256, bar);
                 cp4z(&wb.xn[st][r], a.key_norm + row, true);
@@ -386,8 +296,8 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
         }
         cp_mbar_arrive_noinc(bar);
         issued++;
-        pcur += nr;
-        plan();
+        P0 = P1;
+        plan_next(P1);
     };
 
     float acc[8][NT][4];
@@ -424,7 +334,8 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
             }
         }
         __syncwarp();  // the previous unit's readers of wb.c are done
-        *reinterpret_cast<float4*>(&wb.c[4 * lane]) = __ldg(reinterpret_cast<const float4*>(a.center + u * HD) + lane);
+        const float4 cv = __ldg(reinterpret_cast<const float4*>(a.center + u * HD) + lane);
+        *reinterpret_cast<float4*>(&wb.c[4 * lane]) = make_float4(-cv.x, -cv.y, -cv.z, -cv.w);
         __syncwarp();
         // |q_g|^2: lanes 4g .. 4g+3 hold head g's 128 elements
         sq += __shfl_xor_sync(0xffffffffu, sq, 1);
@@ -434,7 +345,7 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
         qn1 = __shfl_sync(0xffffffffu, qn, 4 * (h1 & 7));
     };
 
-    // leave unit u: record (m, s, a) of this warp -> parts[u + kw]; the last warp of u merges
+    // leave unit u: record (m, s, a) of this warp -> parts[u + kw] (merged by merge_kernel)
     auto flush = [&](int64_t u) {
         float* rec = a.parts + (size_t)(u + kw) * G * PREC;
 #pragma unroll
@@ -468,77 +379,14 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
             if (h0 < G) __stcg(reinterpret_cast<float2*>(rec + h0 * PREC), make_float2(m0, s0));
             if (h1 < G) __stcg(reinterpret_cast<float2*>(rec + h1 * PREC), make_float2(m1, s1));
         }
-        __syncwarp();
-        const int64_t k_lo = owner_of(pref[u], E, Wa), k_hi = owner_of(pref[u + 1] - 1, E, Wa);
-        const uint32_t np = (uint32_t)(k_hi - k_lo + 1);
-        uint32_t old = 0;
-        if (lane == 0)
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.unit_ctr + u) : "memory");
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old != np - 1) return;
-        __syncwarp();
-        // last warp of the unit: merge records u + k_lo .. u + k_hi in fixed order, head by head
-        const float* pu0 = a.parts + (size_t)(u + k_lo) * G * PREC;
-        const int64_t b = u / a.Hkv, hkv = u % a.Hkv, qh0 = b * a.Hq + hkv * G;
-        const int nrec = (int)np;
-#pragma unroll 1
-        for (int g = 0; g < G; g++) {
-            float M = -INFINITY, S = 0.0f;
-            float4 A = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll 1
-            for (int c0 = 0; c0 < nrec; c0 += MB) {
-                const int nr = min(MB, nrec - c0);
-                float4 av[MB];
-#pragma unroll
-                for (int jj = 0; jj < MB; jj++)
-                    av[jj] = jj < nr ? __ldcg(reinterpret_cast<const float4*>(pu0 + ((size_t)(c0 + jj) * G + g) * PREC +
-                                                                            4) +
-                                              lane)
-                                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                const float2 hd = lane < nr ? __ldcg(reinterpret_cast<const float2*>(pu0 + ((size_t)(c0 + lane) * G + g) *
-                                                                                              PREC))
-                                            : make_float2(-INFINITY, 0.0f);
-                float Mn = hd.x;
-#pragma unroll
-                for (int m = 16; m >= 1; m >>= 1) Mn = fmaxf(Mn, __shfl_xor_sync(0xffffffffu, Mn, m));
-                Mn = fmaxf(Mn, M);
-                const float fo = M == -INFINITY ? 0.0f : __expf(M - Mn);
-                const float fc = hd.x == -INFINITY ? 0.0f : __expf(hd.x - Mn);
-                S = S * fo + warp_sum_f(fc * hd.y);
-                A.x *= fo, A.y *= fo, A.z *= fo, A.w *= fo;
-#pragma unroll
-                for (int jj = 0; jj < MB; jj++) {
-                    const float fj = __shfl_sync(0xffffffffu, fc, jj);
-                    A.x = fmaf(fj, av[jj].x, A.x);
-                    A.y = fmaf(fj, av[jj].y, A.y);
-                    A.z = fmaf(fj, av[jj].z, A.z);
-                    A.w = fmaf(fj, av[jj].w, A.w);
-                }
-                M = Mn;
-            }
-            const int64_t row = qh0 + g;
-            if (a.out) {
-                const float inv = S > 0.0f ? 1.0f / S : 0.0f;
-                *reinterpret_cast<float4*>(a.out + row * HD + 4 * lane) = make_float4(A.x * inv, A.y * inv, A.z * inv,
-                                                                                      A.w * inv);
-            }
-            if (a.partial) {
-                float* pp = a.partial + row * PART;
-                *reinterpret_cast<float2*>(pp + 2 + 4 * lane) = make_float2(A.x, A.y);
-                *reinterpret_cast<float2*>(pp + 4 + 4 * lane) = make_float2(A.z, A.w);
-                if (lane == 0) pp[0] = M, pp[1] = S;
-            }
-            if (lane == 0) {
-                if (a.s_count) a.s_count[row] = __ldcg(a.hcnt + row);
-                if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
-            }
-        }
-        if (lane == 0) a.unit_ctr[u] = 0u;
     };
 
-    plan();
+    plan_next(P0);
+    plan_next(P1);
+    stamp(3);
 #pragma unroll 1
     for (int i = 0; i < NST; i++) issue();
+    stamp(4);
     int64_t cur_u = -1;
     reset_state();
 #pragma unroll 1
@@ -555,6 +403,7 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
             load_unit(su);
         }
         mbar_wait(&wb.bar[st], (uint32_t)((computed / NST) & 1));
+        if (computed == 0) stamp(5);
         const uint8_t* Kt = wb.k[st];
         const uint8_t* Vt = wb.v[st];
 
@@ -572,10 +421,10 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
                 const float2 ca = *reinterpret_cast<const float2*>(&wb.c[16 * ks + 2 * t4]);
                 const float2 cb = *reinterpret_cast<const float2*>(&wb.c[16 * ks + 2 * t4 + 8]);
                 uint32_t xf[4];
-                xf[0] = xbar_pair(af[0], ca.x, ca.y);
-                xf[1] = xbar_pair(af[1], ca.x, ca.y);
-                xf[2] = xbar_pair(af[2], cb.x, cb.y);
-                xf[3] = xbar_pair(af[3], cb.x, cb.y);
+                xf[0] = xbar_pair(af[0], ca);
+                xf[1] = xbar_pair(af[1], ca);
+                xf[2] = xbar_pair(af[2], cb);
+                xf[3] = xbar_pair(af[3], cb);
                 mma16816(dx, xf, qf[ks][0], qf[ks][1]);
             }
         }
@@ -612,7 +461,7 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
             __syncwarp();
             for (int e = lane; e < base; e += 32) {
                 const float p = 1.0f - acosf(wb.items[e]) * 0.3183098861837907f;
-                wb.items[e] = log_sampling_prob(p, a.K, a.L, a.minc);
+                wb.items[e] = log_sampling_prob_lut(a.lutab, p, a.K, a.L, a.minc);
             }
             __syncwarp();
 #pragma unroll
@@ -723,7 +572,72 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
         computed++;
         issue();  // refill the stage just consumed
     }
+    stamp(6);
+    if (tl && lane == 0) tl[11] = (unsigned long long)computed;
+    stamp(7);
     if (cur_u >= 0) flush(cur_u);
+    stamp(10);
+}
+
+// ============================================================================ merge
+// CTA per (sequence, query head), thread per dimension: the log-sum-exp merge of the unit's warp records
+// in record order ("recursive attention"): M = max m_j, S = sum s_j e^{m_j - M},
+// A = sum a_j e^{m_j - M}, o = A / S.  PDL: waits for the estimator grid.
+template <int G>
+__global__ void __launch_bounds__(HD) merge_kernel(EstArgs a) {
+    constexpr int RB = 16;  // records per load round (all loads of a round in flight together)
+    __shared__ int hsum[HD / 32];
+    const int64_t row = blockIdx.x, b = row / a.Hq, hq = row % a.Hq;
+    const int64_t g = hq % G, u = b * a.Hkv + hq / G;
+    const int d = threadIdx.x, lane = d & 31;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // |S_g| = sum over the unit's pieces (select step)
+    int hc = 0;
+    for (int64_t c = d; c < a.nchunks; c += HD) hc += __ldcg(a.hpc + row * a.nchunks + c);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) hc += __shfl_xor_sync(0xffffffffu, hc, m);
+    if (lane == 0) hsum[d >> 5] = hc;
+    const int2 rr = __ldcg(a.urec + u);
+    const float* base = a.parts + ((size_t)(u + rr.x) * G + g) * PREC;
+    const size_t stride = (size_t)G * PREC;
+    const int np = rr.y;
+    float M = -INFINITY, S = 0.0f, A = 0.0f;
+#pragma unroll 1
+    for (int j0 = 0; j0 < np; j0 += RB) {
+        float mj[RB], sj[RB], aj[RB];
+#pragma unroll
+        for (int j = 0; j < RB; j++) {
+            const bool ok = j0 + j < np;
+            const float* rp = base + (size_t)(j0 + j) * stride;
+            mj[j] = ok ? __ldcg(rp) : -INFINITY;
+            sj[j] = ok ? __ldcg(rp + 1) : 0.0f;
+            aj[j] = ok ? __ldcg(rp + 4 + d) : 0.0f;
+        }
+        float Mn = M;
+#pragma unroll
+        for (int j = 0; j < RB; j++) Mn = fmaxf(Mn, mj[j]);
+        const float fo = M == -INFINITY ? 0.0f : __expf(M - Mn);
+        S *= fo;
+        A *= fo;
+#pragma unroll
+        for (int j = 0; j < RB; j++) {
+            const float f = mj[j] == -INFINITY ? 0.0f : __expf(mj[j] - Mn);
+            S = fmaf(f, sj[j], S);
+            A = fmaf(f, aj[j], A);
+        }
+        M = Mn;
+    }
+    if (a.out) a.out[row * HD + d] = S > 0.0f ? A * (1.0f / S) : 0.0f;
+    if (a.partial) {
+        float* pp = a.partial + row * PART;
+        pp[2 + d] = A;
+        if (d == 0) pp[0] = M, pp[1] = S;
+    }
+    __syncthreads();
+    if (d == 0) {
+        if (a.s_count) a.s_count[row] = hsum[0] + hsum[1] + hsum[2] + hsum[3];
+        if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
+    }
 }
 
 }  // namespace v7
@@ -733,16 +647,17 @@ static size_t al128e(size_t x) { return (x + 127) & ~(size_t)127; }
 
 size_t estimate_layout(EstArgs& a, int G) {
     (void)G;
-    const size_t units = (size_t)(a.B * a.Hkv);
-    a.off_wbuf = (int)al128e((units + 1) * 8);
+    const size_t pieces = (size_t)(a.B * a.Hkv * (a.nchunks + 1));
+    a.off_wbuf = (int)al128e((pieces + 1) * 4);
     return a.off_wbuf + sizeof(v7::WBuf) * v7::NW;
 }
 
 template <int G>
 static int launch_select_g(const EstArgs& a, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.B * a.Hkv));
-    cfg.blockDim = dim3(v7::SEL_WARPS * 32);
+    const int64_t pieces = a.B * a.Hkv * a.nchunks;
+    cfg.gridDim = dim3((unsigned)((pieces + v7::SEL_WPB - 1) / v7::SEL_WPB));
+    cfg.blockDim = dim3(v7::SEL_WPB * 32);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute attr;
@@ -787,8 +702,35 @@ static int launch_estimate_g(EstArgs a, int nsm, int max_smem, cudaStream_t st) 
     return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
+template <int G>
+static int launch_merge_g(const EstArgs& a, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.B * a.Hq));
+    cfg.blockDim = dim3(HD);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, v7::merge_kernel<G>, a);
+    count_launch(1);
+    return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
+int launch_est_merge(const EstArgs& a, cudaStream_t st) {
+    switch ((int)(a.Hq / a.Hkv)) {
+        case 1: return launch_merge_g<1>(a, st);
+        case 2: return launch_merge_g<2>(a, st);
+        case 4: return launch_merge_g<4>(a, st);
+        case 8: return launch_merge_g<8>(a, st);
+    }
+    return MAGICPIG_EINVAL;
+}
+
 int launch_estimate(const EstArgs& a, int nsm, int max_smem, cudaStream_t st) {
-    if (a.B * a.Hkv > EST_MAX_UNITS || a.n_local >= (1 << 24)) return MAGICPIG_EINVAL;
+    if (a.B * a.Hkv * (a.nchunks + 1) > EST_MAX_PIECES || a.n_local >= (1 << 24)) return MAGICPIG_EINVAL;
     switch ((int)(a.Hq / a.Hkv)) {
         case 1: return launch_estimate_g<1>(a, nsm, max_smem, st);
         case 2: return launch_estimate_g<2>(a, nsm, max_smem, st);

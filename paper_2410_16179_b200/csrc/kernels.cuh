@@ -28,7 +28,7 @@ int launch_hash_gemm(const uint8_t* xt, const uint8_t* wt, const float* xnorm, c
                      uint32_t* status, float* dbg_acc, cudaStream_t st);
 
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
-                   uint32_t* status, cudaStream_t st);
+                   uint32_t* status, cudaStream_t st, int K = 0, int L = 0, int minc = 2, float* lutab = nullptr);
 
 struct DecodeArgs {
     const uint16_t* q;
@@ -83,17 +83,6 @@ int launch_collision_counts(const uint32_t* qbits, const uint32_t* codes, int64_
                             int64_t n_local, int K, int L, int KLw, int KLq, int64_t nchunks, uint16_t* counts,
                             cudaStream_t st);
 
-// ---- decode v6: Query (dense scan6 or bucketed bucket_mark) -> S bitmaps -> estimator (attend)
-struct ScanArgs {
-    const uint32_t* qbits;
-    const uint32_t* codes;
-    uint32_t* sbits;              // [B][Hq][ceil(n/32)]
-    int64_t B, Hkv, Hq, n_local, nchunks, tiles;
-    int K, L, KL, KLw, KLq, ngroups, minc;
-    int nsw, depth, off_qx, off_qbw, off_part;  // set by scan6_layout
-};
-size_t scan6_layout(ScanArgs& a, int G, int max_smem);
-int launch_scan6(const ScanArgs& a, int nsm, int max_smem, cudaStream_t st);
 
 struct AttendArgs {
     const uint16_t* q;
@@ -130,9 +119,9 @@ struct EstArgs {
     int64_t B, Hkv, Hq, n_local, seq_offset, n_global, nchunks;
     int K, L, minc, sink, local;
     int off_wbuf;                 // set by estimate_layout
-    uint32_t* ents;               // [units][n_local] key | head bits << 24 (union_g S_g, ascending)
-    int32_t* ucnt;                // [units] entries of the unit (D only)
-    int32_t* hcnt;                // [B*Hq] |S_g|
+    uint32_t* ents;               // [units][nchunks][1024] per piece: key | head bits << 24 (union_g S_g)
+    int32_t* pcnt;                // [units][nchunks] entries of each piece (D only)
+    int32_t* hpc;                 // [B*Hq][nchunks] |S_g| of each piece
     uint32_t* s_mask;             // debug: S_g restricted to D
     uint32_t* weighted;           // debug: (head, key) pairs that received a finite weight
     float* out;
@@ -141,11 +130,35 @@ struct EstArgs {
     uint32_t* unit_ctr;
     float* parts;
     uint32_t* status;
+    unsigned long long* timeline;  // debug: [grid * EST_WARPS][16] %globaltimer stamps per warp, or NULL
+    int2* urec;                    // [units] (first record slot k_lo, record count) for the merge kernel
+    const float* lutab;            // ln u(p) table (LUT_N + 1 entries over [LUT_P0, 1]), filled by the encode
 };
-constexpr int EST_WARPS = 8;      // warps per estimator CTA
-constexpr int EST_MAX_UNITS = 4096;
+#ifndef MP_EST_WARPS
+#define MP_EST_WARPS 8
+#endif
+constexpr int EST_WARPS = MP_EST_WARPS;  // warps per estimator CTA
+constexpr int EST_MAX_PIECES = 12288;  // units * (chunks + 1): the estimator's piece prefix in smem
 int launch_select(const EstArgs& a, cudaStream_t st);
 size_t estimate_layout(EstArgs& a, int G);
 int launch_estimate(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
+int launch_est_merge(const EstArgs& a, cudaStream_t st);
+
+// ---- decode v6: Query (dense scan6 or bucketed bucket_mark) -> S bitmaps -> estimator (attend)
+struct ScanArgs {
+    const uint32_t* qbits;
+    const uint32_t* codes;
+    uint32_t* sbits;              // [B][Hq][ceil(n/32)]
+    int64_t B, Hkv, Hq, n_local, nchunks, tiles;
+    int K, L, KL, KLw, KLq, ngroups, minc;
+    int nsw, depth, off_qx, off_qbw, off_part;  // set by scan6_layout
+    int fuse;                     // 1: also emit the v7 piece lists (select fused into the scan)
+    EstArgs est;                  //    ... with these outputs
+};
+size_t scan6_layout(ScanArgs& a, int G, int max_smem);
+int launch_scan6(const ScanArgs& a, int nsm, int max_smem, cudaStream_t st);
+
+
+
 
 }  // namespace mp

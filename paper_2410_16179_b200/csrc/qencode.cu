@@ -2,141 +2,166 @@
 // qbar = [q, 0] (reading R4): only the first 128 rows of W meet non-zero
 // query entries.  Bit j = [exact(q . W_j) > 0] (R6).
 //
-// fp32 accumulation of exact bf16 x bf16 products with a certified sign test,
-// fp64 and exact-integer fallbacks for the rare near-zero dots (see kernel).
+// A small dense contraction Q [B*Hq][128] x W [128][K*L] on tensor cores
+// (mma.sync bf16: every product q_d W_dj is exact, fp32 accumulate).  The same
+// contraction of |q| and |W| bounds sum_d |q_d W_dj|; a sign is certified when
+// |acc| > 2^-16 * bound (the fp32 tensor-core accumulation error over 8 k-steps
+// is below 2^-19 of the bound), otherwise the thread recomputes that dot in
+// fp64 (certified at 2^-44) and, failing that, in exact integers.
+//
+// CTA = 32 columns (one packed query-code word) x 128 query heads; warp w owns
+// heads 16w .. 16w+15 (one m16 tile) and all 4 n8 tiles.  W is read once per
+// CTA (fp32 -> bf16, exact by the bf16-representable contract) and staged
+// column-major in shared memory; q fragments come straight from global memory.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace mp {
 
-constexpr int QE_COLS = 32;   // columns per CTA (one warp-wide ballot word)
-constexpr int QE_HPB = 8;     // query heads per CTA
+constexpr int QE_COLS = 32;    // columns per CTA = one qbits word
+constexpr int QE_HEADS = 128;  // query heads per CTA
 constexpr int QE_THREADS = 256;
+constexpr int QE_WP = HD + 8;  // smem pitch (bf16) of a staged W column: conflict-free fragment loads
 
-// CTA = 32 columns x 8 heads; warp w: heads 4*(w%2) .. +3, d-quarter w/2; lane = column.
-// fp32 products are exact (bf16 x bf16); fp32 sums certify the sign when
-// |acc| > 2^-16 sum|q_d W_dj| (error <= 65 * 2^-24 * sum|.|); otherwise the
-// warp recomputes that dot in fp64 (certified at 2^-44) and, failing that, in
-// exact integers.
+__device__ __forceinline__ void qe_mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __restrict__ q, int64_t BHq,
                                                              const float* __restrict__ W, int KL, int KLw,
-                                                             uint32_t* __restrict__ qbits, uint32_t* status) {
-    // let the dependent decode kernel launch now: it streams codes while we encode
+                                                             uint32_t* __restrict__ qbits, uint32_t* status,
+                                                             int K, int L, int minc, float* __restrict__ lutab) {
+    // let the dependent Query kernel launch now (it waits for the codes with griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ float ws[HD][QE_COLS];
-    __shared__ __align__(16) float qs[HD][QE_HPB];
-    __shared__ __align__(16) float qa[HD][QE_HPB];
-    __shared__ float pacc[3][QE_HPB][QE_COLS], pbnd[3][QE_HPB][QE_COLS];
+    __shared__ int lut_todo;
+    if (lutab) {
+        // the estimator's ln u(p) table (Eq.) in fp64, spread over the CTAs; kept in the workspace
+        // and refilled only when (K, L, min_collisions) change: header word = key, next word = arrivals
+        uint32_t* hdr = reinterpret_cast<uint32_t*>(lutab + LUT_N + 2);
+        const uint32_t want = 1u + (((uint32_t)K * 2048u + (uint32_t)L) << 1) + (uint32_t)(minc - 1);
+        if (threadIdx.x == 0) lut_todo = __ldcg(hdr) != want;
+        __syncthreads();
+        if (lut_todo) {
+            const int nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+            for (int i = bid * QE_THREADS + threadIdx.x; i <= LUT_N; i += nb * QE_THREADS)
+                lutab[i] = (float)log_sampling_prob_d((double)LUT_P0 + (double)i * (1.0 - (double)LUT_P0) / LUT_N,
+                                                      K, L, minc);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(hdr + 1, 1u) == (uint32_t)nb - 1) {  // last CTA: the table is complete
+                    hdr[1] = 0u;
+                    __threadfence();
+                    atomicExch(hdr, want);
+                }
+            }
+        }
+    }
+    __shared__ __align__(16) uint16_t wsm[QE_COLS][QE_WP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j0 = blockIdx.x * QE_COLS;
-    const int64_t h0 = (int64_t)blockIdx.y * QE_HPB;
-    {   // all loads in flight before any store (16 W values + 8 q values per thread)
-        constexpr int NW = HD * QE_COLS / QE_THREADS, NQ = HD * QE_HPB / QE_THREADS;
-        float wv[NW];
-        uint16_t qv[NQ];
+    {   // W[d][j0 .. j0+31] -> bf16, column-major in smem (all 16 loads per thread in flight first)
+        constexpr int NL = HD * QE_COLS / QE_THREADS;
+        float wv[NL];
 #pragma unroll
-        for (int i = 0; i < NW; i++) {
+        for (int i = 0; i < NL; i++) {
             const int e = tid + i * QE_THREADS, d = e / QE_COLS, c = e % QE_COLS;
             wv[i] = (j0 + c < KL) ? __ldg(W + (int64_t)d * KL + j0 + c) : 0.0f;
         }
 #pragma unroll
-        for (int i = 0; i < NQ; i++) {
-            const int e = tid + i * QE_THREADS, h = e / HD, d = e % HD;
-            qv[i] = (h0 + h < BHq) ? __ldg(q + (h0 + h) * HD + d) : (uint16_t)0;
+        for (int i = 0; i < NL; i++) {
+            const int e = tid + i * QE_THREADS, d = e / QE_COLS, c = e % QE_COLS;
+            wsm[c][d] = (uint16_t)(__float_as_uint(wv[i]) >> 16);  // exact: W is bf16-representable
         }
+    }
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int64_t hbase = (int64_t)blockIdx.y * QE_HEADS + warp * 16;
+    const int64_t ha = hbase + g4, hb = hbase + g4 + 8;
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(q + (ha < BHq ? ha : 0) * HD);
+    const uint32_t* qb = reinterpret_cast<const uint32_t*>(q + (hb < BHq ? hb : 0) * HD);
+    uint32_t af[8][4];
 #pragma unroll
-        for (int i = 0; i < NW; i++) {
-            const int e = tid + i * QE_THREADS;
-            ws[e / QE_COLS][e % QE_COLS] = wv[i];
-        }
-#pragma unroll
-        for (int i = 0; i < NQ; i++) {
-            const int e = tid + i * QE_THREADS, h = e / HD, d = e % HD;
-            const float f = bf2f(qv[i]);
-            qs[d][h] = f;
-            qa[d][h] = fabsf(f);
-        }
+    for (int ks = 0; ks < 8; ks++) {
+        const int w0 = (16 * ks + 2 * t4) >> 1;
+        af[ks][0] = ha < BHq ? __ldg(qa + w0) : 0u;
+        af[ks][1] = hb < BHq ? __ldg(qb + w0) : 0u;
+        af[ks][2] = ha < BHq ? __ldg(qa + w0 + 4) : 0u;
+        af[ks][3] = hb < BHq ? __ldg(qb + w0 + 4) : 0u;
     }
     __syncthreads();
-    const int hs = warp & 1, dq = warp >> 1;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, bnd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 16
-    for (int dd = 0; dd < HD / 4; dd++) {
-        const int d = dq * (HD / 4) + dd;
-        const float w = ws[d][lane];
-        const float wa = fabsf(w);
-        const float4 q4 = *reinterpret_cast<const float4*>(&qs[d][hs * 4]);
-        const float4 a4 = *reinterpret_cast<const float4*>(&qa[d][hs * 4]);
-        acc[0] = fmaf(q4.x, w, acc[0]);
-        acc[1] = fmaf(q4.y, w, acc[1]);
-        acc[2] = fmaf(q4.z, w, acc[2]);
-        acc[3] = fmaf(q4.w, w, acc[3]);
-        bnd[0] = fmaf(a4.x, wa, bnd[0]);
-        bnd[1] = fmaf(a4.y, wa, bnd[1]);
-        bnd[2] = fmaf(a4.z, wa, bnd[2]);
-        bnd[3] = fmaf(a4.w, wa, bnd[3]);
-    }
-    if (dq > 0) {
+    float acc[4][4], bnd[4][4];
 #pragma unroll
-        for (int t = 0; t < 4; t++) {
-            pacc[dq - 1][hs * 4 + t][lane] = acc[t];
-            pbnd[dq - 1][hs * 4 + t][lane] = bnd[t];
+    for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) acc[nt][i] = bnd[nt][i] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ks++) {
+        uint32_t aa[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) aa[i] = af[ks][i] & 0x7fff7fffu;  // |q| (exact)
+#pragma unroll
+        for (int nt = 0; nt < 4; nt++) {
+            const uint16_t* wc = &wsm[nt * 8 + g4][16 * ks + 2 * t4];
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wc);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wc + 8);
+            qe_mma(acc[nt], af[ks], b0, b1);
+            qe_mma(bnd[nt], aa, b0 & 0x7fff7fffu, b1 & 0x7fff7fffu);
         }
     }
-    __syncthreads();
-    if (dq > 0) return;
-    const int j = j0 + lane;
-    const bool live = j < KL;
+    // bits: element (row, col) = (g4 | g4 + 8, nt * 8 + 2 t4 + i) in acc[nt][(row >= 8) * 2 + i]
+    uint32_t wa = 0u, wb = 0u;
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
-        const int h = hs * 4 + t;
-        const float s = ((acc[t] + pacc[0][h][lane]) + pacc[1][h][lane]) + pacc[2][h][lane];
-        const float bb = ((bnd[t] + pbnd[0][h][lane]) + pbnd[1][h][lane]) + pbnd[2][h][lane];
-        int bit = s > 0.0f;
-        const bool unsure = live && (h0 + h < BHq) && !(fabsf(s) > 0x1p-16f * bb);
-        uint32_t um = __ballot_sync(0xffffffffu, unsure);
-        while (um) {  // rare: warp-cooperative fp64 recomputation of column (j0 + src)
-            const int src = __ffs(um) - 1;
-            um &= um - 1;
-            double sd = 0.0, bd = 0.0;
+    for (int nt = 0; nt < 4; nt++) {
 #pragma unroll
-            for (int r = 0; r < HD / 32; r++) {
-                const int d = lane + 32 * r;
-                const double pq = (double)qs[d][h] * (double)ws[d][src];
-                sd += pq;
-                bd += fabs(pq);
-            }
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) {
-                sd += __shfl_xor_sync(0xffffffffu, sd, m);
-                bd += __shfl_xor_sync(0xffffffffu, bd, m);
-            }
-            int b2;
-            if (fabs(sd) > 0x1p-44 * bd) {
-                b2 = sd > 0.0;
-            } else {
-                b2 = 0;
-                if (lane == 0) {
-                    uint16_t xa[HD], wb[HD];
-                    for (int d = 0; d < HD; d++) {
-                        xa[d] = q[(h0 + h) * HD + d];
-                        wb[d] = (uint16_t)(__float_as_uint(ws[d][src]) >> 16);
-                    }
-                    b2 = exact_dot_sign_bf16(xa, wb, HD, status) > 0;
+        for (int e = 0; e < 4; e++) {
+            const int col = nt * 8 + 2 * t4 + (e & 1);
+            const int64_t h = (e >> 1) ? hb : ha;
+            const bool live = j0 + col < KL && h < BHq;
+            const float s = acc[nt][e];
+            int bit = s > 0.0f;
+            if (live && !(fabsf(s) > 0x1p-16f * bnd[nt][e])) {
+                // rare: this thread recomputes the dot in fp64, then exactly
+                double sd = 0.0, bd = 0.0;
+                for (int d = 0; d < HD; d++) {
+                    const double pq = (double)bf2f(q[h * HD + d]) * (double)bf2f(wsm[col][d]);
+                    sd += pq;
+                    bd += fabs(pq);
                 }
-                b2 = __shfl_sync(0xffffffffu, b2, 0);
+                if (fabs(sd) > 0x1p-44 * bd) {
+                    bit = sd > 0.0;
+                } else {
+                    uint16_t xa[HD], wv[HD];
+                    for (int d = 0; d < HD; d++) {
+                        xa[d] = q[h * HD + d];
+                        wv[d] = wsm[col][d];
+                    }
+                    bit = exact_dot_sign_bf16(xa, wv, HD, status) > 0;
+                }
             }
-            if (lane == src) bit = b2;
+            if (bit && live) {
+                if (e >> 1) wb |= 1u << col;
+                else wa |= 1u << col;
+            }
         }
-        const uint32_t word = __ballot_sync(0xffffffffu, bit && live);
-        if (lane == 0 && h0 + h < BHq && (j0 >> 5) < KLw) qbits[(h0 + h) * KLw + (j0 >> 5)] = word;
+    }
+    wa |= __shfl_xor_sync(0xffffffffu, wa, 1);
+    wa |= __shfl_xor_sync(0xffffffffu, wa, 2);
+    wb |= __shfl_xor_sync(0xffffffffu, wb, 1);
+    wb |= __shfl_xor_sync(0xffffffffu, wb, 2);
+    if (t4 == 0) {
+        if (ha < BHq) qbits[ha * KLw + (j0 >> 5)] = wa;
+        if (hb < BHq) qbits[hb * KLw + (j0 >> 5)] = wb;
     }
 }
 
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
-                   uint32_t* status, cudaStream_t st) {
-    dim3 grid((unsigned)((KL + QE_COLS - 1) / QE_COLS), (unsigned)((BHq + QE_HPB - 1) / QE_HPB));
-    qencode_kernel<<<grid, QE_THREADS, 0, st>>>(q, BHq, W, KL, KLw, qbits, status);
+                   uint32_t* status, cudaStream_t st, int K, int L, int minc, float* lutab) {
+    dim3 grid((unsigned)KLw, (unsigned)((BHq + QE_HEADS - 1) / QE_HEADS));
+    qencode_kernel<<<grid, QE_THREADS, 0, st>>>(q, BHq, W, KL, KLw, qbits, status, K, L, minc, lutab);
     count_launch(1);
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }

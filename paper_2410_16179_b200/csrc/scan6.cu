@@ -17,6 +17,7 @@
 // combined per chunk in shared memory (one barrier per chunk, double-buffered).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "pieces.cuh"
 
 namespace mp {
 namespace v6 {
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scan6_kernel(ScanArgs a) {
     uint32_t* qx = reinterpret_cast<uint32_t*>(dsm + a.off_qx);           // [ncolsP][G] match masks
     uint32_t* qbw = reinterpret_cast<uint32_t*>(dsm + a.off_qbw);         // [G][KLw] packed query bits
     uint32_t* s_part = reinterpret_cast<uint32_t*>(dsm + a.off_part);     // [2][nsw][G][2][32]
+    __shared__ uint32_t s_fin[2][8][32];                                   // fused select: S_g words per chunk
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NSW = a.nsw, NTH = NSW * 32;
@@ -175,7 +177,18 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scan6_kernel(ScanArgs a) {
                 f1 |= b1;
             }
             const int64_t wi = chunk * 32 + lane;
-            if (wi < nwb) a.sbits[(qh0 + g) * nwb + wi] = a.minc == 1 ? f1 : f2;
+            if (a.fuse) s_fin[par][g][lane] = a.minc == 1 ? f1 : f2;
+            else if (wi < nwb) a.sbits[(qh0 + g) * nwb + wi] = a.minc == 1 ? f1 : f2;
+        }
+        if (a.fuse && warp < G) {
+            // select fused into the scan: the union of the unit's heads over this chunk -> its piece list
+            if (G > 1) asm volatile("bar.sync 1, %0;" ::"r"(G * 32) : "memory");
+            if (warp == 0) {
+                uint32_t sg[G];
+#pragma unroll
+                for (int g = 0; g < G; g++) sg[g] = s_fin[par][g][lane];
+                v7::emit_piece<G>(a.est, v7::static_ranges(a.est), u, chunk, qh0, lane, sg);
+            }
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -195,7 +208,7 @@ size_t scan6_layout(ScanArgs& a, int G, int max_smem) {
     fixed += al128s((size_t)G * a.KLw * 4);
     const size_t o_part = fixed;
     fixed += al128s((size_t)2 * v6::NSW_MAX * G * 2 * 32 * 4);
-    const size_t budget = (size_t)max_smem - 256;
+    const size_t budget = (size_t)max_smem - 256 - 2048;  // static smem of the kernel (s_fin)
     if (fixed >= budget) return 0;
     size_t avail = budget - fixed;
     if (avail > (size_t)v6::RING_BUDGET) avail = v6::RING_BUDGET;

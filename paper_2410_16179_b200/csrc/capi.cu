@@ -362,8 +362,9 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
     const int kver = g_decode_kernel.load();
-    if ((kver % 10 == 6 && !timeline) || kver % 10 == 7) {
-        const bool v7 = kver % 10 == 7 && B * Hkv * (g.nchunks + 1) <= EST_MAX_PIECES && n_local < (1 << 24);
+    if ((kver % 10 == 6 && !timeline) || kver % 10 == 7 || kver % 10 == 8) {
+        const bool v7 = (kver % 10 == 7 || kver % 10 == 8) && B * Hkv * (g.nchunks + 1) <= EST_MAX_PIECES &&
+                        n_local < (1 << 24);
         EstArgs ea;
         memset(&ea, 0, sizeof(ea));
         ea.q = q, ea.center = center, ea.key_norm = key_norm, ea.k = k, ea.v = v, ea.sbits = w.sbits;
@@ -406,7 +407,13 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
             }
             if ((stages & 2) && !fused) rc = launch_select(ea, st);
             if (rc || !(stages & 4)) return rc;
-            rc = launch_estimate(ea, num_sms(), max_smem_optin(), st);
+            // kernel 8: the tcgen05 estimator (TMA gather4 tiles) when its layout fits, else kernel 7's
+            if (kver % 10 == 8 && estimate8_ok(ea, max_smem_optin())) {
+                if (grid_out) *grid_out = num_sms();  // timeline rows (one per CTA)
+                rc = launch_estimate8(ea, num_sms(), max_smem_optin(), st);
+            } else {
+                rc = launch_estimate(ea, num_sms(), max_smem_optin(), st);
+            }
             return rc ? rc : launch_est_merge(ea, st);
         }
         // estimator over S_g u T
@@ -448,7 +455,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
 }
 
 extern "C" int magicpig_debug_set_decode_kernel(int version) {
-    if (version % 10 < 4 || version % 10 > 7) return MAGICPIG_EINVAL;
+    if (version % 10 < 4 || version % 10 > 8) return MAGICPIG_EINVAL;
     g_decode_kernel.store(version);
     return MAGICPIG_OK;
 }

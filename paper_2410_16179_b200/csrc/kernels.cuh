@@ -143,6 +143,8 @@ int launch_select(const EstArgs& a, cudaStream_t st);
 size_t estimate_layout(EstArgs& a, int G);
 int launch_estimate(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
 int launch_est_merge(const EstArgs& a, cudaStream_t st);
+bool estimate8_ok(const EstArgs& a, int max_smem);
+int launch_estimate8(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
 
 // ---- decode v6: Query (dense scan6 or bucketed bucket_mark) -> S bitmaps -> estimator (attend)
 struct ScanArgs {

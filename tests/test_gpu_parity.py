@@ -20,13 +20,13 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-3
 
 
-@pytest.fixture(params=[7, 6, 5], ids=["k7", "k6", "k5"], autouse=True)
+@pytest.fixture(params=[8, 7, 6, 5], ids=["k8", "k7", "k6", "k5"], autouse=True)
 def decode_kernel(request):
-    """Every parity test runs on three decode paths: 7 = Query kernel + select kernel (ordered
-    S_g u T lists) + balanced estimator kernel (the default), 6 = Query kernel + estimator kernel
-    with a producer warp, and 5 = the persistent fused kernel (which falls back to the
-    cluster-per-chunk kernel 4 when its shared memory does not fit); they must agree with the
-    oracle independently."""
+    """Every parity test runs on four decode paths: 8 = Query kernel + select (per-piece S_g u T
+    lists) + the tcgen05 estimator (TMA gather4 tiles, TMEM accumulators), 7 = the same with the
+    mma.sync estimator (every warp a contiguous range), 6 = Query kernel + estimator kernel with a
+    producer warp, and 5 = the persistent fused kernel (which falls back to the cluster-per-chunk
+    kernel 4 when its shared memory does not fit); they must agree with the oracle independently."""
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device (no fallback)")
     pkg = _pkg()

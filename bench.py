@@ -68,12 +68,16 @@ def _peaks():
 
 
 def _traffic(kernel_key):
-    """DRAM bytes per launch of a kernel from the committed ncu --set full summary (or None)."""
+    """DRAM bytes per launch of a kernel (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
+    ncu --set full summary (tools/ncu_summary2.py), captured at the same workload, or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         try:
             with open(p) as f:
-                return json.load(f).get(kernel_key, {}).get("dram_bytes_per_launch")
+                d = json.load(f)
+            e = d.get(kernel_key)
+            return {"bytes": e["dram_bytes_per_launch"], "source": f"profiles/ncu_summary.json ({d.get('tag')}, "
+                    f"{e.get('capture')})"} if e else None
         except Exception:
             return None
     return None
@@ -376,17 +380,36 @@ def measure_decode(rw, path, dev, tW, peaks, k, v, q, graph_steps=64, group=None
         return fn
 
     res = {"step_us": _graph_time(step, R, graph_steps)}
+    choice = B_.decode_kernel_choice(cfg, Bn, Hq, Hkv, n, path == "buckets")
+    res["decode_kernel"] = choice
     if rw.mode != "sequence":
         B_.encode_queries(cfg, reps.qs[0], tW, ws)
-        res["stage_us"] = {"query": _graph_time(stage(1), R, graph_steps),
-                           "select": _graph_time(stage(2), R, graph_steps),
-                           "estimate": _graph_time(stage(4), R, graph_steps)}
-        # stage 2 and 4 above re-use replica 0's S bitmaps / lists for every replica's K/V: same bytes moved
         kern = {}
-        for nm in ("query", "select", "estimate"):
-            us = res["stage_us"][nm]
-            kern[nm] = {"us": us, "alg_MB": ab[nm] / 1e6, "GBs": ab[nm] / us / 1e3, "frac": ab[nm] / us / 1e3 /
-                        peaks["hbm"]}
+        if choice == 5:  # one fused kernel (scan or bitmap Query + estimator + unit merge)
+            def dec(r):
+                d = B_.decode_buckets_encoded if path == "buckets" else B_.decode_encoded
+                d(cfg, reps.qs[r], reps.tables(r) if path == "buckets" else reps.codes(r), reps.mps[r].buf.center,
+                  reps.mps[r].buf.key_norm, reps.ks[r], reps.vs[r], 0, n, ws, out=out)
+            us = _graph_time(dec, R, graph_steps)
+            names = {"decode": "decode5_kernel" + (" (+ bucket_mark_kernel)" if path == "buckets" else "")}
+            ab["decode"] = ab["step"] - Bn * Hq * 256
+            kern["decode"] = {"us": us, "alg_MB": ab["decode"] / 1e6}
+        else:
+            # stages 2 and 4 re-use replica 0's lists for every replica's K/V: the same bytes are moved
+            kern["query"] = {"us": _graph_time(stage(1), R, graph_steps)}
+            if path == "buckets":
+                kern["select"] = {"us": _graph_time(stage(2), R, graph_steps)}
+            else:  # the select step is fused into the dense scan
+                ab["query"] += ab["select"]
+            kern["estimate"] = {"us": _graph_time(stage(4), R, graph_steps), "note": "estimate + merge kernels"}
+            names = {"query": "bucket_mark_kernel" if path == "buckets" else "scan6_kernel (select fused)",
+                     "select": "select_kernel", "estimate": "estimate_kernel" if choice == 7 else "estimate8_kernel"}
+            for nm in kern:
+                kern[nm]["alg_MB"] = ab[nm] / 1e6
+        for nm, kd in kern.items():
+            kd["GBs"] = kd["alg_MB"] * 1e6 / kd["us"] / 1e3
+            kd["frac"] = kd["GBs"] / peaks["hbm"]
+            kd["kernel"] = names[nm]
         res["kernels"] = kern
     res.update(n=n, B=Bn, Hq=Hq, Hkv=Hkv, K=wl.K, L=wl.L, path=path, replicas=R, union_rows=n_union, static_rows=nT,
                alg_bytes=ab, sampled_fraction=float(scount.float().mean()) / max(n - nT, 1), status=status,
@@ -590,10 +613,9 @@ def run_ours(args):
     if "kernels" in m:
         dom = max(m["kernels"], key=lambda kn: m["kernels"][kn]["us"])
         kd = m["kernels"][dom]
-        names = {"query": "bucket_mark_kernel" if path == "buckets" else "scan6_kernel",
-                 "select": "select_kernel", "estimate": "estimate_kernel"}
+        kname = kd["kernel"].split(" ")[0]
         roof = {"bound": "hbm", "achieved": kd["GBs"], "peak": peaks["hbm"], "unit": "GB/s", "frac": kd["frac"],
-                "traffic": _traffic(names[dom]), "kernel": names[dom], "kernel_us": kd["us"],
+                "traffic": _traffic(kname), "kernel": kd["kernel"], "kernel_us": kd["us"],
                 "alg_bytes_per_launch": kd["alg_MB"] * 1e6, "peak_source": peak_src,
                 "step": {"alg_bytes": m["alg_bytes"]["step"], "us": m["step_us"], "GBs": m["step_GBs"],
                          "frac": m["step_frac"]}}
@@ -693,6 +715,7 @@ def run_ours(args):
                        "alg_bytes_per_step": m["alg_bytes"]["step"], "status": m["status"]},
             "roofline": roof,
             "kernels": m.get("kernels"),
+            "decode_kernel": m.get("decode_kernel"),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(q_host.numel() * 2),
                     "d2h_bytes_per_step": int(out_host.numel() * 4), "ms_per_step": e2e_ms,

@@ -13,7 +13,9 @@
  *     as uint16_t bit patterns.  All work is enqueued on `stream`
  *     (a cudaStream_t; NULL = legacy default stream) and is asynchronous.
  *   - The caller owns every buffer, including the workspace; the library
- *     never allocates or frees device memory and keeps no global state.
+ *     never allocates or frees device memory.  Its only process-wide state is a
+ *     launch counter and the debug decode-kernel selector
+ *     (magicpig_debug_set_decode_kernel; default 0 = automatic choice).
  *   - Return value: MAGICPIG_OK (0) or a negative error code (argument and
  *     launch errors).  Errors that can only be detected on the device
  *     (exact-range violations, fixup-list overflow) are OR-ed into a status
@@ -215,6 +217,24 @@ int magicpig_decode_buckets_encoded(const magicpig_config* cfg, const uint16_t* 
  * (fixed order j = 0..P-1, so every rank gets bit-identical results). */
 int magicpig_merge_partials(const float* parts, int P, int64_t BH, float* out, void* stream);
 
+/* Decode-time append (the decoded token's key joins the cache; the
+ * local window of the static set T moves with it): hashes the m new keys of every
+ * (sequence, kv head) unit, k_new [B][Hkv][m][128] bf16, which become positions
+ * n_old .. n_old+m-1, with the index's FROZEN centering vector and MIPS radius
+ * (center, r2 from the build; reading R3: an appended key with |x|^2 > r^2 gets
+ * the MIPS coordinate 0), exactly like magicpig_build_tables: their key_norm
+ * entries and their code bits (exact signs, sign(0) = 0).  codes and key_norm
+ * must already be laid out for n_old + m keys per unit (codes: the layout of
+ * magicpig_codes_words(.., n_old + m); key_norm: [B][Hkv][n_old + m]); the caller
+ * moves the existing entries when the layout grows (a new 1024-key chunk, or the
+ * key_norm row stride).  The token that leaves the local window becomes a dynamic
+ * key by position alone at the next decode (n_global = n_old + m); its code was
+ * computed when it was built or appended.  ws: any library workspace (its status
+ * word collects MAGICPIG_STATUS_INEXACT).  Returns 0 or an error code. */
+int magicpig_append_keys(const magicpig_config* cfg, const uint16_t* k_new, int64_t m, int64_t B, int64_t Hkv,
+                         int64_t n_old, const float* W, const float* center, const int64_t* r2, uint32_t* codes,
+                         float* key_norm, void* ws, size_t ws_bytes, void* stream);
+
 /* One whole decode step from HOST memory (the serving call): copies q_host
  * [B][Hq][128] bf16 [host; pinned memory makes the copy asynchronous] into the
  * workspace, encodes it, decodes it over the dense codes (tables ==
@@ -321,9 +341,15 @@ int magicpig_debug_build_phases(const magicpig_config* cfg, const uint16_t* k, i
                                 void* const* events);
 
 /* Selects the decode kernel for subsequent decode calls of this process (a debug
- * knob for A/B measurement; default 6): 6 = Query kernel (dense code scan, or the
- * bucketed tables) writing per-head S bitmaps, then the estimator kernel (all warps
- * gather 16-row slabs independently); 5 = persistent warp-specialised fused kernel
+ * knob for A/B measurement).  0 (default) = automatic: kernel 5 for small decodes
+ * (at most two 1024-key chunk tiles per SM: latency-bound, one fused launch), else
+ * kernel 7.  7 = Query kernel (dense code scan with the select step fused, or the
+ * bucketed tables + select kernel) emitting per-piece S_g u T lists, then the
+ * balanced mma.sync estimator (every warp a contiguous range of the concatenated
+ * lists) and the unit merge kernel; 8 = the same with the tcgen05 estimator (TMA-
+ * free cp.async tiles in 128B-swizzled layout, TMEM accumulators); 6 = Query
+ * kernel writing per-head S bitmaps, then an estimator with a producer warp;
+ * 5 = persistent warp-specialised fused kernel
  * (one CTA per SM over a contiguous tile range; used whenever its shared-memory
  * layout fits, else 4), 4 = one thread-block cluster per 1024-key chunk.  Both
  * compute the same S bit for bit.  For kernel 5 the timeline slots are clock64
@@ -331,6 +357,11 @@ int magicpig_debug_build_phases(const magicpig_config* cfg, const uint16_t* k, i
  * gather batch, 4 unit merge start, 5 unit merge end, 6 gather done.
  * Returns 0 or MAGICPIG_EINVAL. [host] */
 int magicpig_debug_set_decode_kernel(int version);
+
+/* The decode kernel generation (4..8) the next decode call with these shapes will run
+ * (resolves the automatic choice of kernel 0).  Returns it, or MAGICPIG_EINVAL. [host] */
+int magicpig_debug_decode_kernel_choice(const magicpig_config* cfg, int64_t B, int64_t Hq, int64_t Hkv,
+                                        int64_t n_local, int buckets);
 
 /* Message for an error code. [host] */
 const char* magicpig_strerror(int err);

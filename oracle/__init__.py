@@ -96,6 +96,20 @@ def lib():
         L.oracle_decode_indexed.restype = _i
         L.oracle_merge_partials.argtypes = [_i, _i, _p, _p]
         L.oracle_merge_partials.restype = _i
+        L.oracle_softmax_f64.argtypes = [_i, _p, _p]
+        L.oracle_softmax_f64.restype = None
+        L.oracle_expectation.argtypes = [_i, _i, _p, _p, _p]
+        L.oracle_expectation.restype = None
+        L.oracle_topk_estimate.argtypes = [_i, _i, _p, _p, _i, _p]
+        L.oracle_topk_estimate.restype = _i
+        L.oracle_oracle_sampling.argtypes = [_i, _i, _p, _p, _i, _p, _p]
+        L.oracle_oracle_sampling.restype = _i
+        L.oracle_oracle_sampling_std.argtypes = [_i, _i, _p, _p, _i, _p]
+        L.oracle_oracle_sampling_std.restype = None
+        L.oracle_expected_unique.argtypes = [_i, _p, _i]
+        L.oracle_expected_unique.restype = _d
+        L.oracle_append_keys.argtypes = [_i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p]
+        L.oracle_append_keys.restype = _i
         _lib = L
     return _lib
 
@@ -253,6 +267,56 @@ def estimate(q, k, v, sel, logu):
     return {"out": out, "m": m.value, "s": s.value, "a": a, "any": bool(any_)}
 
 
+# ---------------------------------------------------------------- estimator-quality harness (NEXT-3)
+def softmax_f64(x: np.ndarray) -> np.ndarray:
+    x = _c(x, np.float64)
+    w = np.zeros_like(x)
+    lib().oracle_softmax_f64(int(x.size), _ptr(x), _ptr(w))
+    return w
+
+
+def expectation(w: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """o = wV (P:779); v [n][d] (or [n] for scalars)."""
+    w, v = _c(w, np.float64), _c(v.reshape(len(w), -1), np.float64)
+    n, d = v.shape
+    out = np.zeros(d, np.float64)
+    lib().oracle_expectation(n, d, _ptr(w), _ptr(v), _ptr(out))
+    return out
+
+
+def topk_estimate(w: np.ndarray, v: np.ndarray, m: int) -> np.ndarray:
+    """TopK attention, renormalized over the m largest weights."""
+    w, v = _c(w, np.float64), _c(v.reshape(len(w), -1), np.float64)
+    n, d = v.shape
+    out = np.zeros(d, np.float64)
+    lib().oracle_topk_estimate(n, d, _ptr(w), _ptr(v), int(m), _ptr(out))
+    return out
+
+
+def oracle_sampling(w: np.ndarray, v: np.ndarray, uniforms: np.ndarray):
+    """Oracle sampling estimation with the caller's uniform variates -> (estimate, |S|)."""
+    w, v, u = _c(w, np.float64), _c(v.reshape(len(w), -1), np.float64), _c(uniforms, np.float64)
+    n, d = v.shape
+    out = np.zeros(d, np.float64)
+    uniq = lib().oracle_oracle_sampling(n, d, _ptr(w), _ptr(v), int(u.size), _ptr(u), _ptr(out))
+    return out, int(uniq)
+
+
+def oracle_sampling_std(w: np.ndarray, v: np.ndarray, B: int) -> np.ndarray:
+    """Theorem 1: per-coordinate standard deviation of the oracle-sampling estimate with budget B."""
+    w, v = _c(w, np.float64), _c(v.reshape(len(w), -1), np.float64)
+    n, d = v.shape
+    out = np.zeros(d, np.float64)
+    lib().oracle_oracle_sampling_std(n, d, _ptr(w), _ptr(v), int(B), _ptr(out))
+    return out
+
+
+def expected_unique(w: np.ndarray, B: int) -> float:
+    """Theorem 2: E|S| = sum_i (1 - (1 - w_i)^B)."""
+    w = _c(w, np.float64)
+    return float(lib().oracle_expected_unique(int(w.size), _ptr(w), int(B)))
+
+
 def merge_partials(parts: np.ndarray) -> np.ndarray:
     parts = _c(parts, np.float64)
     P, dd = parts.shape
@@ -308,6 +372,33 @@ def build_unit(k, W, K: int, L: int, center: int = 1, mips: int = 1, sink: int =
             "mips": mips, "sink": sink, "local": local, "W": W}
 
 
+def build_unit_q(k, W, K: int, L: int, center: int = 1, mips: int = 1, sink: int = 4, local: int = 64):
+    """build_unit plus the exact fixed-point MIPS radius r2_q (a Python int), needed to append keys."""
+    idx = build_unit(k, W, K, L, center, mips, sink, local)
+    idx["r2_q"] = key_transform(k, sink, local, center, mips)["r2_q"]
+    return idx
+
+
+def append_keys(index, k_new):
+    """Decode-time append (NEXT-2): hash k_new [m][d] with the index's frozen c and r^2 and return a new index
+    for n + m keys (the local window rolls by position at decode time)."""
+    k_new = _c(k_new, np.uint16)
+    m, d = k_new.shape
+    K, L, mips = index["K"], index["L"], index["mips"]
+    dp = d + (1 if mips else 0)
+    xbar = np.zeros((m, dp), np.uint16)
+    n2 = np.zeros(m, np.float64)
+    codes = np.zeros((m, L), np.uint16)
+    r2q = index["r2_q"] & ((1 << 128) - 1)
+    pair = np.array([r2q & ((1 << 64) - 1), r2q >> 64], np.uint64)
+    st = lib().oracle_append_keys(m, d, K, L, mips, _ptr(k_new), _ptr(index["W"]), _ptr(_c(index["c"], np.float32)),
+                                  _ptr(pair), _ptr(xbar), _ptr(n2), _ptr(codes))
+    out = dict(index)
+    out.update(xbar=np.vstack([index["xbar"], xbar]), n2=np.concatenate([index["n2"], n2]),
+               codes=np.vstack([index["codes"], codes]), status=st)
+    return out
+
+
 def decode_indexed(index, k, v, q, min_collisions: int = 2):
     """Decode half of Alg. 1 for one unit given oracle.build_unit(...) output."""
     k, v = _c(k, np.uint16), _c(v, np.uint16)
@@ -318,11 +409,12 @@ def decode_indexed(index, k, v, q, min_collisions: int = 2):
     G = q.shape[0]
     out = np.zeros((G, d), np.float64)
     s_count = np.zeros(G, np.int32)
+    in_s = np.zeros((G, n), np.uint8)
     st = lib().oracle_decode_indexed(n, d, G, index["K"], index["L"], index["mips"], min_collisions,
                                      index["sink"], index["local"], _ptr(k), _ptr(v), _ptr(q), _ptr(index["W"]),
                                      _ptr(index["xbar"]), _ptr(index["n2"]), _ptr(index["codes"]), _ptr(out),
-                                     None, _ptr(s_count), None, None, None, None)
-    return {"out": out, "s_count": s_count, "status": st}
+                                     None, _ptr(s_count), None, _ptr(in_s), None, None)
+    return {"out": out, "s_count": s_count, "in_s": in_s, "status": st}
 
 
 def decode_batch(k, v, q, W, K, L, center=1, mips=1, min_collisions=2, sink=4, local=64,

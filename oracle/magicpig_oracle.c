@@ -666,3 +666,149 @@ int oracle_merge_partials(int P, int d, const double *parts, double *out) {
     for (int t = 0; t < d; t++) out[t] /= S;
     return 1;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Estimator-quality harness: the estimators the paper
+ * compares, over a normalized attention distribution w [n] (sum 1) and values
+ * v [n][d], all in double (o = wV).                               */
+
+/* w = Softmax(x). */
+void oracle_softmax_f64(int n, const double *x, double *w) {
+    double m = -INFINITY, z = 0.0;
+    for (int i = 0; i < n; i++)
+        if (x[i] > m) m = x[i];
+    for (int i = 0; i < n; i++) {
+        w[i] = exp(x[i] - m);
+        z += w[i];
+    }
+    for (int i = 0; i < n; i++) w[i] /= z;
+}
+
+/* Exact output o = wV. */
+void oracle_expectation(int n, int d, const double *w, const double *v, double *out) {
+    for (int j = 0; j < d; j++) out[j] = 0.0;
+    for (int i = 0; i < n; i++)
+        for (int j = 0; j < d; j++) out[j] += w[i] * v[(size_t)i * d + j];
+}
+
+/* TopK attention: the m indices r_1..r_m with the largest w (ties:
+ * lower index first), o = sum_j w_{r_j} v_{r_j} / sum_j w_{r_j}.  Returns m. */
+int oracle_topk_estimate(int n, int d, const double *w, const double *v, int m, double *out) {
+    if (m > n) m = n;
+    if (m < 0) m = 0;
+    unsigned char *taken = (unsigned char *)calloc((size_t)(n > 0 ? n : 1), 1);
+    double den = 0.0;
+    for (int j = 0; j < d; j++) out[j] = 0.0;
+    for (int r = 0; r < m; r++) { /* plain selection: the largest untaken weight */
+        int best = -1;
+        for (int i = 0; i < n; i++)
+            if (!taken[i] && (best < 0 || w[i] > w[best])) best = i;
+        taken[best] = 1;
+        den += w[best];
+        for (int j = 0; j < d; j++) out[j] += w[best] * v[(size_t)best * d + j];
+    }
+    for (int j = 0; j < d; j++) out[j] = den > 0.0 ? out[j] / den : 0.0;
+    free(taken);
+    return m;
+}
+
+/* Oracle sampling estimation (Definition): B indices drawn iid from
+ * w -- draw j is the first index whose cumulative weight exceeds uniforms[j]
+ * (uniforms in [0, 1), supplied by the caller) -- and o = (1/B) sum_j v_{i_j}
+ * = sum_{i in S} (f_i / B) v_i.  Returns |S| (unique draws). */
+int oracle_oracle_sampling(int n, int d, const double *w, const double *v, int B, const double *uniforms,
+                           double *out) {
+    double *cdf = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    int *f = (int *)calloc((size_t)(n > 0 ? n : 1), sizeof(int));
+    double c = 0.0;
+    for (int i = 0; i < n; i++) {
+        c += w[i];
+        cdf[i] = c;
+    }
+    for (int b = 0; b < B; b++) {
+        int lo = 0, hi = n - 1; /* first i with cdf[i] > u (the last index if rounding leaves u >= cdf) */
+        while (lo < hi) {
+            int mid = (lo + hi) / 2;
+            if (cdf[mid] > uniforms[b]) hi = mid;
+            else lo = mid + 1;
+        }
+        f[lo]++;
+    }
+    int uniq = 0;
+    for (int j = 0; j < d; j++) out[j] = 0.0;
+    for (int i = 0; i < n; i++) {
+        if (!f[i]) continue;
+        uniq++;
+        for (int j = 0; j < d; j++) out[j] += ((double)f[i] / (double)B) * v[(size_t)i * d + j];
+    }
+    free(cdf);
+    free(f);
+    return uniq;
+}
+
+/* Theorem 1: the oracle-sampling estimate is unbiased with per-
+ * coordinate variance Var_w(v_j) / B; std[j] = sqrt((E_w[v_j^2] - E_w[v_j]^2) / B). */
+void oracle_oracle_sampling_std(int n, int d, const double *w, const double *v, int B, double *std) {
+    for (int j = 0; j < d; j++) {
+        double m1 = 0.0, m2 = 0.0;
+        for (int i = 0; i < n; i++) {
+            const double x = v[(size_t)i * d + j];
+            m1 += w[i] * x;
+            m2 += w[i] * x * x;
+        }
+        const double var = m2 - m1 * m1;
+        std[j] = sqrt((var > 0.0 ? var : 0.0) / (double)B);
+    }
+}
+
+/* Theorem 2: E|S| = sum_i (1 - (1 - w_i)^B) (each index is absent
+ * from B iid draws with probability (1 - w_i)^B), bounded by 1 + B (1 - max_i w_i). */
+double oracle_expected_unique(int n, const double *w, int B) {
+    double e = 0.0;
+    for (int i = 0; i < n; i++) e += -expm1((double)B * log1p(-w[i]));
+    return e;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Decode-time append (P:171 on-device local window, P:619
+ * 64 local tokens): a new key is hashed with the index's FROZEN centering
+ * vector c and MIPS radius r^2 (reading R3: c and r are taken over D at build
+ * time; an appended key with |x|^2 > r^2 gets s = 0, i.e. r^2 - n2 clamped at
+ * 0), exactly as oracle_key_transform + oracle_encode_keys do for built keys:
+ *   x = bf16_rn(fl32(k - c)),  n2q = sum_d q(x_d^2),
+ *   s = bf16_rn(sqrt_rn(fl64(max(r2q - n2q, 0) 2^-64)))   (mips),
+ *   codes = SimHash of xbar = [x, s].
+ * r2_q: the frozen radius as the (lo, hi) int128 pair of oracle_key_transform.
+ * Outputs xbar [m][d+mips], n2 [m] (= fl64(n2q 2^-64)), codes [m][L].  The
+ * token leaving the local window becomes a dynamic key by position alone
+ * (oracle_is_static with the new n), its code already exists (R16).        */
+int oracle_append_keys(int m, int d, int K, int L, int mips, const uint16_t *k_new, const float *W,
+                       const float *c, const uint64_t *r2_q, uint16_t *xbar, double *n2, uint16_t *codes) {
+    if (m < 0 || d <= 0 || K < 1 || K > 16 || L < 1) return OR_EINVAL;
+    int dp = d + (mips ? 1 : 0);
+    int rc = oracle_check_w(W, (int64_t)dp * K * L);
+    if (rc) return rc;
+    const i128 r2q = (i128)(((unsigned __int128)r2_q[1] << 64) | (unsigned __int128)r2_q[0]);
+    int inexact = 0;
+    for (int i = 0; i < m; i++) {
+        i128 acc = 0;
+        for (int j = 0; j < d; j++) {
+            double kv = oracle_bf16_to_double(k_new[(size_t)i * d + j]);
+            if (fabs(kv) >= ABS_LIMIT) inexact = 1;
+            double hi, lo;
+            two_sum(kv, -(double)c[j], &hi, &lo);
+            uint16_t xb = oracle_bf16_from_double((double)f32_round_pair(hi, lo));
+            xbar[(size_t)i * dp + j] = xb;
+            double xv = oracle_bf16_to_double(xb);
+            if (fabs(xv) >= ABS_LIMIT) inexact = 1;
+            acc += fix_of(xv * xv);
+        }
+        n2[i] = oracle_fix_to_double(acc);
+        if (mips) {
+            double diff = r2q > acc ? oracle_fix_to_double(r2q - acc) : 0.0;
+            xbar[(size_t)i * dp + d] = oracle_bf16_from_double(sqrt(diff));
+        }
+    }
+    oracle_encode_keys(m, dp, xbar, W, K, L, codes);
+    return inexact ? OR_EINEXACT : OR_OK;
+}

@@ -61,6 +61,7 @@ _SIGS = {
     "magicpig_decode_buckets_encoded": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p,
                                          _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_set_decode_kernel": ([_i], _i),
+    "magicpig_debug_decode_kernel_choice": ([_p, _i64, _i64, _i64, _i64, _i], _i),
     "magicpig_debug_decode_sets": ([_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p,
                                     _p, _p, _sz, _p], _i),
     "magicpig_export_codes": ([_p, _p, _i64, _i64, _i64, _p, _p], _i),
@@ -70,6 +71,7 @@ _SIGS = {
     "magicpig_debug_hash_acc": ([_p, _p, _i64, _p, _p, _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_decode_timeline": ([_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _p,
                                         _sz, _p], _i64),
+    "magicpig_append_keys": ([_p, _p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _sz, _p], _i),
     "magicpig_decode_host": ([_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _sz, _p], _i),
     "magicpig_debug_decode_stage": ([_p, _i, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _sz, _p],
                                     _i),
@@ -268,6 +270,14 @@ def decode_host(cfg, q_host, codes, tables, center, key_norm, k, v, W, out_host,
                                       C.c_void_p(out_host.data_ptr()), _ptr(ws), ws.numel(), _stream()), "decode_host")
 
 
+def append_keys(cfg, k_new, n_old, W, center, r2, codes, key_norm, ws):
+    """Hash the new keys k_new [B][Hkv][m][128] (positions n_old ..) with the frozen c, r^2 into codes /
+    key_norm already laid out for n_old + m keys."""
+    B, Hkv, m, _ = k_new.shape
+    _check(lib().magicpig_append_keys(_cfg(cfg), _ptr(k_new), m, B, Hkv, n_old, _ptr(W), _ptr(center), _ptr(r2),
+                                      _ptr(codes), _ptr(key_norm), _ptr(ws), ws.numel(), _stream()), "append_keys")
+
+
 def merge_partials(parts, out):
     P, BH, _ = parts.shape
     _check(lib().magicpig_merge_partials(_ptr(parts), P, BH, _ptr(out), _stream()), "merge_partials")
@@ -358,9 +368,16 @@ def debug_build_phases(cfg, k, W, center, r2, codes, key_norm, key_sum, count, w
 
 
 def set_decode_kernel(version: int):
-    """Debug knob: 6 = Query kernel + estimator kernel (default), 5 = persistent fused kernel,
-    4 = cluster-per-chunk."""
+    """Debug knob (magicpig.h): 0 = automatic (default), 4..8 = a specific decode kernel generation."""
     _check(lib().magicpig_debug_set_decode_kernel(int(version)), "set_decode_kernel")
+
+
+def decode_kernel_choice(cfg, B, Hq, Hkv, n, buckets=False) -> int:
+    """The decode kernel generation the next decode with these shapes runs (resolves the automatic choice)."""
+    rc = int(lib().magicpig_debug_decode_kernel_choice(_cfg(cfg), B, Hq, Hkv, n, int(bool(buckets))))
+    if rc < 0:
+        _check(rc, "decode_kernel_choice")
+    return rc
 
 
 def launch_count() -> int:

@@ -353,4 +353,78 @@ int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
+// ---------------------------------------------------------------------------
+// Decode-time append: keys n_old .. n_old + m - 1 of every unit hashed with the index's
+// frozen c and r^2 (reading R3; s = 0 when |x|^2 > r^2), exactly as the build does: xbar, |xbar| (key_norm),
+// and one bit per projection column, bit = [exact xbar . W_j > 0] (R6) written into the bit-plane
+// codes (layout for n_old + m keys).  CTA per (new key, unit): warp 0 forms xbar in shared memory; then
+// thread per column: fp64 sum of the exact bf16 x bf16 products, certified when |sum| > 2^-44 sum |.|
+// (the fp64 error over 129 terms is below 2^-45 of it), else the exact integer sign.
+__global__ void __launch_bounds__(256) append_keys_kernel(const uint16_t* __restrict__ k_new, int64_t m,
+                                                          int64_t n_old, int mips, const float* __restrict__ W,
+                                                          int KL, int KLq, int64_t nchunks,
+                                                          const float* __restrict__ center,
+                                                          const int64_t* __restrict__ r2, uint32_t* __restrict__ codes,
+                                                          float* __restrict__ key_norm, uint32_t* status) {
+    __shared__ uint16_t xs[HD + 8];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t i = blockIdx.x, unit = blockIdx.y;
+    const int64_t n_new = n_old + m, pos = n_old + i;
+    const int dp = HD + (mips ? 1 : 0);
+    if (tid < 32) {
+        const float4 c = reinterpret_cast<const float4*>(center + unit * HD)[lane];
+        const uint2 kr = reinterpret_cast<const uint2*>(k_new + (unit * m + i) * HD)[lane];
+        uint32_t a = 0, b = 0;
+        bool bad = false;
+        const u128 n2 = warp_sum_u128(transform4(kr, c, a, b, bad));
+        if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
+        reinterpret_cast<uint2*>(xs)[lane] = make_uint2(a, b);
+        if (lane == 0) {
+            uint16_t sv = 0;
+            if (mips) {
+                const i128 diff = ld_q64(r2 + unit * 2) - (i128)n2;
+                sv = diff > 0 ? d2bf_rn_pos(sqrt(q64_to_double(diff))) : (uint16_t)0;
+            }
+            xs[HD] = sv;
+            const float sf = bf2f(sv);
+            key_norm[unit * n_new + pos] = (float)sqrt(q64_to_double((i128)n2) + (double)sf * (double)sf);
+        }
+    }
+    __syncthreads();
+    const int64_t chunk = pos >> 10, blk = (pos >> 5) & 31;
+    const uint32_t bit = 1u << (pos & 31);
+    uint32_t* cu = codes + (unit * nchunks + chunk) * (int64_t)KLq * 128;
+    for (int j = tid; j < KLq * 4; j += blockDim.x) {
+        int sg = 0;
+        if (j < KL) {
+            double s = 0.0, sa = 0.0;
+            for (int d = 0; d < dp; d++) {
+                const double pr = (double)bf2f(xs[d]) * (double)__ldg(W + (int64_t)d * KL + j);
+                s += pr;
+                sa += fabs(pr);
+            }
+            if (fabs(s) > 0x1p-44 * sa) {
+                sg = s > 0.0;
+            } else {
+                uint16_t wv[HD + 1];
+                for (int d = 0; d < dp; d++) wv[d] = (uint16_t)(__float_as_uint(__ldg(W + (int64_t)d * KL + j)) >> 16);
+                sg = exact_dot_sign_bf16(xs, wv, dp, status) > 0;
+            }
+        }
+        uint32_t* w = cu + (((int64_t)(j >> 2)) * 32 + blk) * 4 + (j & 3);
+        if (sg) atomicOr(w, bit);
+        else atomicAnd(w, ~bit);
+    }
+}
+
+int launch_append_keys(const uint16_t* k_new, int64_t m, int64_t units, int64_t n_old, int mips, const float* W,
+                       int KL, int KLq, int64_t nchunks, const float* center, const int64_t* r2, uint32_t* codes,
+                       float* key_norm, uint32_t* status, cudaStream_t st) {
+    if (m < 1 || units < 1) return 0;
+    append_keys_kernel<<<dim3((unsigned)m, (unsigned)units), 256, 0, st>>>(k_new, m, n_old, mips, W, KL, KLq, nchunks,
+                                                                          center, r2, codes, key_norm, status);
+    count_launch(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+}
+
 }  // namespace mp

@@ -1,5 +1,5 @@
 // capi.cu -- the C ABI (include/magicpig.h): validation, workspace layout,
-// launch sequencing.  No allocation, no global state besides a launch counter.
+// launch sequencing.  No allocation; process-wide state: a launch counter and the debug kernel selector.
 #include <atomic>
 #include <cstring>
 
@@ -34,11 +34,10 @@ static int max_smem_optin() {
     return n;
 }
 
-// decode kernel selection (debug knob, magicpig_debug_set_decode_kernel): 6 = Query kernel (dense
-// scan6 or bucket_mark) -> S bitmaps -> estimator kernel (attend.cu) (default); 5 = persistent
-// warp-specialised fused kernel (falls back to 4 when its shared memory does not fit), 4 = one
-// cluster per chunk.  5 and 4 are kept as A/B arms; all compute the same S bit for bit.
-static std::atomic<int> g_decode_kernel{7};
+// decode kernel selection (debug knob, magicpig_debug_set_decode_kernel; see magicpig.h): 0 = automatic
+// (5 for small decodes, else 7), 4..8 = a specific kernel generation (A/B arms); all compute the same S
+// bit for bit.
+static std::atomic<int> g_decode_kernel{0};
 
 static bool cfg_ok(const magicpig_config* c) {
     if (!c) return false;
@@ -259,6 +258,17 @@ int magicpig_build_tables(const magicpig_config* cfg, const uint16_t* k, int64_t
                             n_local, w.n_pad, g.nchunks, w.KD, g.KL, w.NT, g.KLq, w.status, nullptr, st);
 }
 
+int magicpig_append_keys(const magicpig_config* cfg, const uint16_t* k_new, int64_t m, int64_t B, int64_t Hkv,
+                         int64_t n_old, const float* W, const float* center, const int64_t* r2, uint32_t* codes,
+                         float* key_norm, void* ws, size_t ws_bytes, void* stream) {
+    if (!cfg_ok(cfg) || m < 0 || B < 1 || Hkv < 1 || n_old < 0 || !shape_ok(B, Hkv, n_old + m, 0, n_old + m))
+        return MAGICPIG_EINVAL;
+    if (m > 0 && (!k_new || !W || !center || !r2 || !codes || !key_norm || !ws || ws_bytes < 4)) return MAGICPIG_EINVAL;
+    const Geom g = make_geom(cfg->K, cfg->L, n_old + m);
+    return launch_append_keys(k_new, m, B * Hkv, n_old, cfg->mips, W, g.KL, g.KLq, g.nchunks, center, r2, codes,
+                              key_norm, (uint32_t*)ws, S(stream));
+}
+
 int magicpig_build_index(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,
                          const float* W, float* center, int64_t* r2, uint32_t* codes, float* key_norm,
                          int64_t* key_sum, int64_t* count, void* ws, size_t ws_bytes, void* stream) {
@@ -285,7 +295,8 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
                        int64_t Hkv, int64_t n_local, int64_t seq_offset, int64_t n_global, float* out,
                        float* partial, int32_t* s_count, uint32_t* s_mask, void* ws, size_t ws_bytes,
                        void* stream, unsigned long long* timeline, int64_t timeline_len, int64_t* grid_out,
-                       const int32_t* tables = nullptr, uint32_t* weighted = nullptr, int stages = 7) {
+                       const int32_t* tables = nullptr, uint32_t* weighted = nullptr, int stages = 7,
+                       int force_kver = -1) {
     if (!cfg_ok(cfg) || !shape_ok(B, Hkv, n_local, seq_offset, n_global)) return MAGICPIG_EINVAL;
     if (Hq < Hkv || Hq % Hkv) return MAGICPIG_EINVAL;
     const int64_t G = Hq / Hkv;
@@ -361,7 +372,15 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     a.parts = w.parts;
     a.chunk_cnt = w.chunk_cnt;
     a.status = w.status;
-    const int kver = g_decode_kernel.load();
+    int kver = force_kver >= 0 ? force_kver : g_decode_kernel.load();
+    if (kver == 0) {
+        // auto (default): small decodes (at most two 1024-key chunk tiles per SM) are latency-bound -> the
+        // persistent fused kernel 5 (one launch after the encode); larger ones -> kernel 7 (Query kernel,
+        // select, the balanced estimator, the unit merge), which scales with the sampled rows
+        DecodeArgs t = a;
+        const bool small = B * Hkv * g.nchunks <= 2 * (int64_t)num_sms() && decode5_layout(t, (int)G, max_smem_optin());
+        kver = small ? 5 : 7;
+    }
     if ((kver % 10 == 6 && !timeline) || kver % 10 == 7 || kver % 10 == 8) {
         const bool v7 = (kver % 10 == 7 || kver % 10 == 8) && B * Hkv * (g.nchunks + 1) <= EST_MAX_PIECES &&
                         n_local < (1 << 24);
@@ -454,8 +473,26 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
     return v5 ? launch_decode5(a, num_sms(), max_smem_optin(), st) : launch_decode(a, st);
 }
 
+extern "C" int magicpig_debug_decode_kernel_choice(const magicpig_config* cfg, int64_t B, int64_t Hq, int64_t Hkv,
+                                                   int64_t n_local, int buckets) {
+    if (!cfg_ok(cfg) || B < 1 || Hkv < 1 || Hq < Hkv || Hq % Hkv || n_local < 1) return MAGICPIG_EINVAL;
+    int kver = g_decode_kernel.load();
+    const Geom g = make_geom(cfg->K, cfg->L, n_local);
+    const int64_t G = Hq / Hkv;
+    if (kver == 0) {
+        DecodeArgs t;
+        memset(&t, 0, sizeof(t));
+        t.K = cfg->K, t.L = cfg->L, t.KL = g.KL, t.KLw = g.KLw, t.KLq = g.KLq, t.ngroups = g.ngroups;
+        t.TG = g.TG, t.QG = g.QG, t.nchunks = g.nchunks, t.B = B, t.Hkv = Hkv, t.Hq = Hq, t.n_local = n_local;
+        const bool small = B * Hkv * g.nchunks <= 2 * (int64_t)num_sms() && decode5_layout(t, (int)G, max_smem_optin());
+        kver = small ? 5 : 7;
+    }
+    (void)buckets;
+    return kver % 10;
+}
+
 extern "C" int magicpig_debug_set_decode_kernel(int version) {
-    if (version % 10 < 4 || version % 10 > 8) return MAGICPIG_EINVAL;
+    if (version != 0 && (version % 10 < 4 || version % 10 > 8)) return MAGICPIG_EINVAL;
     g_decode_kernel.store(version);
     return MAGICPIG_OK;
 }
@@ -556,13 +593,15 @@ int magicpig_debug_decode_sets(const magicpig_config* cfg, const uint16_t* q, in
                                void* ws, size_t ws_bytes, void* stream) {
     if (!W || !weighted || (n_local > 0 && !codes && !tables) || n_local < 1) return MAGICPIG_EINVAL;
     if (!cfg_ok(cfg) || Hq < Hkv || Hkv < 1 || B < 1 || Hq % Hkv) return MAGICPIG_EINVAL;
-    if (g_decode_kernel.load() % 10 < 6) return MAGICPIG_EINVAL;
+    const int kv = g_decode_kernel.load();
+    if (kv != 0 && kv % 10 < 6) return MAGICPIG_EINVAL;  // the weighted-set export exists on kernels 6-8
     if (cudaMemsetAsync(weighted, 0, (size_t)B * Hq * ((n_local + 31) / 32) * 4, S(stream)) != cudaSuccess)
         return MAGICPIG_ECUDA;
     int rc = magicpig_encode_queries(cfg, q, B, Hq, W, ws, ws_bytes, stream);
     if (rc) return rc;
     return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
-                       nullptr, nullptr, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, weighted);
+                       nullptr, nullptr, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, weighted, 7,
+                       kv == 0 ? 7 : kv);
 }
 
 int magicpig_decode_host(const magicpig_config* cfg, const uint16_t* q_host, int64_t Hq, const uint32_t* codes,
@@ -593,9 +632,10 @@ int magicpig_debug_decode_stage(const magicpig_config* cfg, int stage, const uin
                                 const float* key_norm, const uint16_t* k, const uint16_t* v, int64_t B, int64_t Hkv,
                                 int64_t n_local, float* out, void* ws, size_t ws_bytes, void* stream) {
     if (stage < 1 || stage > 7) return MAGICPIG_EINVAL;
-    if (g_decode_kernel.load() % 10 < 6 || n_local < 1) return MAGICPIG_EINVAL;
+    const int kv = g_decode_kernel.load();
+    if ((kv != 0 && kv % 10 < 6) || n_local < 1) return MAGICPIG_EINVAL;
     return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, 0, n_local, out, nullptr, nullptr,
-                       nullptr, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, nullptr, stage);
+                       nullptr, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, nullptr, stage, kv == 0 ? 7 : kv);
 }
 
 int magicpig_debug_build_phases(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,

@@ -718,6 +718,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                 const float w = (z == -INFINITY) ? 0.0f : to_tf32(__expf(z - mn));
                 const float wsum = warp_sum_f(w);
                 f.w[rr][g] = w;
+                __syncwarp();  // every lane has read f.mrun[g] before lane 0 replaces it
                 if (lane == 0) {
                     f.scale[g] = sc;
                     f.srun[g] = f.srun[g] * sc + wsum;

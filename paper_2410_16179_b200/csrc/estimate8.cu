@@ -108,7 +108,9 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ void bar_cw() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
+// named barrier of the compute warps; the two head halves reach it from different instantiations (code
+// addresses) of the compute loop, hence the non-.aligned form
+__device__ __forceinline__ void bar_cw() { asm volatile("barrier.sync 1, %0;" ::"n"(NCT) : "memory"); }
 __device__ __forceinline__ int64_t owner_of(int64_t e, int64_t E, int64_t W) { return ((e + 1) * W - 1) / E; }
 
 template <int G>

@@ -27,6 +27,9 @@ int launch_hash_gemm(const uint8_t* xt, const uint8_t* wt, const float* xnorm, c
                      int64_t n_local, int64_t n_pad, int64_t nchunks, int KD, int KL, int NT, int KLq,
                      uint32_t* status, float* dbg_acc, cudaStream_t st);
 
+int launch_append_keys(const uint16_t* k_new, int64_t m, int64_t units, int64_t n_old, int mips, const float* W,
+                       int KL, int KLq, int64_t nchunks, const float* center, const int64_t* r2, uint32_t* codes,
+                       float* key_norm, uint32_t* status, cudaStream_t st);
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
                    uint32_t* status, cudaStream_t st, int K = 0, int L = 0, int minc = 2, float* lutab = nullptr);
 

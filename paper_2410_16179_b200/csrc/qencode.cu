@@ -37,33 +37,15 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
                                                              int K, int L, int minc, float* __restrict__ lutab) {
     // let the dependent Query kernel launch now (it waits for the codes with griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ int lut_todo;
-    if (lutab) {
-        // the estimator's ln u(p) table (Eq. P:86-91) in fp64, spread over the CTAs; kept in the workspace
-        // and refilled only when (K, L, min_collisions) change: header word = key, next word = arrivals
-        uint32_t* hdr = reinterpret_cast<uint32_t*>(lutab + LUT_N + 2);
-        const uint32_t want = 1u + (((uint32_t)K * 2048u + (uint32_t)L) << 1) + (uint32_t)(minc - 1);
-        if (threadIdx.x == 0) lut_todo = __ldcg(hdr) != want;
-        __syncthreads();
-        if (lut_todo) {
-            const int nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
-            for (int i = bid * QE_THREADS + threadIdx.x; i <= LUT_N; i += nb * QE_THREADS)
-                lutab[i] = (float)log_sampling_prob_d((double)LUT_P0 + (double)i * (1.0 - (double)LUT_P0) / LUT_N,
-                                                      K, L, minc);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                if (atomicAdd(hdr + 1, 1u) == (uint32_t)nb - 1) {  // last CTA: the table is complete
-                    hdr[1] = 0u;
-                    __threadfence();
-                    atomicExch(hdr, want);
-                }
-            }
-        }
-    }
     __shared__ __align__(16) uint16_t wsm[QE_COLS][QE_WP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j0 = blockIdx.x * QE_COLS;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int64_t hbase = (int64_t)blockIdx.y * QE_HEADS + warp * 16;
+    const int64_t ha = hbase + g4, hb = hbase + g4 + 8;
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(q + (ha < BHq ? ha : 0) * HD);
+    const uint32_t* qb = reinterpret_cast<const uint32_t*>(q + (hb < BHq ? hb : 0) * HD);
+    uint32_t af[8][4];
     {   // W[d][j0 .. j0+31] -> bf16, column-major in smem (all 16 loads per thread in flight first)
         constexpr int NL = HD * QE_COLS / QE_THREADS;
         float wv[NL];
@@ -72,25 +54,20 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
             const int e = tid + i * QE_THREADS, d = e / QE_COLS, c = e % QE_COLS;
             wv[i] = (j0 + c < KL) ? __ldg(W + (int64_t)d * KL + j0 + c) : 0.0f;
         }
+        // q fragments: loads in flight together with W's (one global latency)
+#pragma unroll
+        for (int ks = 0; ks < 8; ks++) {
+            const int w0 = (16 * ks + 2 * t4) >> 1;
+            af[ks][0] = ha < BHq ? __ldg(qa + w0) : 0u;
+            af[ks][1] = hb < BHq ? __ldg(qb + w0) : 0u;
+            af[ks][2] = ha < BHq ? __ldg(qa + w0 + 4) : 0u;
+            af[ks][3] = hb < BHq ? __ldg(qb + w0 + 4) : 0u;
+        }
 #pragma unroll
         for (int i = 0; i < NL; i++) {
             const int e = tid + i * QE_THREADS, d = e / QE_COLS, c = e % QE_COLS;
             wsm[c][d] = (uint16_t)(__float_as_uint(wv[i]) >> 16);  // exact: W is bf16-representable
         }
-    }
-    const int g4 = lane >> 2, t4 = lane & 3;
-    const int64_t hbase = (int64_t)blockIdx.y * QE_HEADS + warp * 16;
-    const int64_t ha = hbase + g4, hb = hbase + g4 + 8;
-    const uint32_t* qa = reinterpret_cast<const uint32_t*>(q + (ha < BHq ? ha : 0) * HD);
-    const uint32_t* qb = reinterpret_cast<const uint32_t*>(q + (hb < BHq ? hb : 0) * HD);
-    uint32_t af[8][4];
-#pragma unroll
-    for (int ks = 0; ks < 8; ks++) {
-        const int w0 = (16 * ks + 2 * t4) >> 1;
-        af[ks][0] = ha < BHq ? __ldg(qa + w0) : 0u;
-        af[ks][1] = hb < BHq ? __ldg(qb + w0) : 0u;
-        af[ks][2] = ha < BHq ? __ldg(qa + w0 + 4) : 0u;
-        af[ks][3] = hb < BHq ? __ldg(qb + w0 + 4) : 0u;
     }
     __syncthreads();
     float acc[4][4], bnd[4][4];
@@ -155,6 +132,30 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
     if (t4 == 0) {
         if (ha < BHq) qbits[ha * KLw + (j0 >> 5)] = wa;
         if (hb < BHq) qbits[hb * KLw + (j0 >> 5)] = wb;
+    }
+    __shared__ int lut_todo;
+    if (lutab) {  // after the codes: off the Query kernel's critical path until this grid completes
+        // the estimator's ln u(p) table (Eq. P:86-91) in fp64, spread over the CTAs; kept in the workspace
+        // and refilled only when (K, L, min_collisions) change: header word = key, next word = arrivals
+        uint32_t* hdr = reinterpret_cast<uint32_t*>(lutab + LUT_N + 2);
+        const uint32_t want = 1u + (((uint32_t)K * 2048u + (uint32_t)L) << 1) + (uint32_t)(minc - 1);
+        if (threadIdx.x == 0) lut_todo = __ldcg(hdr) != want;
+        __syncthreads();
+        if (lut_todo) {
+            const int nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+            for (int i = bid * QE_THREADS + threadIdx.x; i <= LUT_N; i += nb * QE_THREADS)
+                lutab[i] = (float)log_sampling_prob_d((double)LUT_P0 + (double)i * (1.0 - (double)LUT_P0) / LUT_N,
+                                                      K, L, minc);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(hdr + 1, 1u) == (uint32_t)nb - 1) {  // last CTA: the table is complete
+                    hdr[1] = 0u;
+                    __threadfence();
+                    atomicExch(hdr, want);
+                }
+            }
+        }
     }
 }
 

@@ -101,6 +101,35 @@ class MagicPIG:
         self.buf.tables = torch.empty((words,), dtype=torch.int32, device=self.buf.codes.device)
         B_.build_buckets(self.cfg, self.buf.codes, Bn, Hkv, n, self.buf.tables)
 
+    def append(self, k_new: torch.Tensor):
+        """Decode-time append: the new keys k_new [B][Hkv][m][128] bf16 become positions
+        n .. n+m-1, hashed with the frozen centering vector and MIPS radius of the build; the local window of
+        the static set rolls with n at the next decode.  The index buffers are re-laid out for n + m keys
+        (plumbing); the bucketed tables, when present, are rebuilt from the codes."""
+        if self.buf is None or self.seq_offset != 0:
+            raise B_.MagicPIGError("append needs an unsharded built index")
+        Bn, Hkv, n = self.shape
+        if k_new.dtype != torch.bfloat16 or k_new.dim() != 4 or tuple(k_new.shape[:2]) != (Bn, Hkv) or \
+                k_new.shape[3] != 128:
+            raise B_.MagicPIGError(f"k_new must be bfloat16 [{Bn}][{Hkv}][m][128]")
+        m = k_new.shape[2]
+        n_new = n + m
+        b = self.buf
+        units = Bn * Hkv
+        w_old, w_new = B_.codes_words(self.cfg, Bn, Hkv, n), B_.codes_words(self.cfg, Bn, Hkv, n_new)
+        if w_new != w_old:  # a new 1024-key chunk per unit: move each unit's chunks to the wider layout
+            codes = torch.zeros((w_new,), dtype=torch.int32, device=b.codes.device)
+            codes.view(units, -1)[:, :w_old // units].copy_(b.codes[:w_old].view(units, -1))
+            b.codes = codes
+        key_norm = torch.empty((Bn, Hkv, n_new), dtype=torch.float32, device=b.key_norm.device)
+        key_norm[:, :, :n].copy_(b.key_norm[:, :, :n])
+        b.key_norm = key_norm
+        ws = self._ws_dec if self._ws_dec is not None else B_.new_workspace(256, k_new.device)
+        B_.append_keys(self.cfg, k_new.contiguous(), n, self.W, b.center, b.r2, b.codes, b.key_norm, ws)
+        self.shape, self.n_global = (Bn, Hkv, n_new), n_new
+        self._build_buckets()
+        return self
+
     def build_sharded(self, k_local: torch.Tensor, seq_offset: int, n_global: int, group=None):
         """Sequence-sharded build: this rank holds keys [seq_offset, seq_offset + n_local)."""
         import torch.distributed as dist

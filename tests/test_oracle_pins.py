@@ -416,3 +416,33 @@ def test_w_must_be_bf16_representable():
     W[0, 0] = np.float32(1.0 + 2.0 ** -20)
     r = oracle.decode_unit(c["k"], c["v"], c["q"], W, 2, 2, 1, 0, 2, 0, 0)
     assert r["status"] == oracle.OR_ENOTREPR
+
+
+# --------------------------------------------------------------------------- x = bf16(fl32(k - c)), wide operands
+def test_centered_key_rounding_when_k_minus_c_is_inexact_in_double():
+    """x_i = bf16_rn(fl32(k_i - c)) (C-2 contract) when |k| / |c| > 2^29: k - c then spans more than
+    53 bits, so the oracle's fp64 difference is inexact and its pair rounding (f32_round_pair, the TwoSum residue
+    branch) decides fl32.  Checked against exact rational rounding (tests/exact_ref.py), with keys near fp32 and
+    bf16 rounding boundaries and centering vectors of both signs."""
+    d = 128
+    rng = np.random.default_rng(29)
+    for trial in range(6):
+        n = 12
+        kf = np.zeros((n, d), np.float32)
+        # dynamic keys (positions 1 .. 10 with sink 1, local 1): tiny values, |D| = 10 -> c has a full mantissa
+        kf[1:11, :] = (rng.integers(-7, 8, (10, d)) * 2.0 ** (-12 - trial)).astype(np.float32)
+        # the static keys carry large values: 2^18 +- a few bf16 ulps, and values just off bf16 midpoints
+        big = 2.0 ** (16 + trial) * (1.0 + rng.integers(0, 128, d) / 128.0)
+        kf[0, :] = big.astype(np.float32) * np.where(rng.random(d) < 0.5, -1.0, 1.0)
+        kf[11, :] = (big * (1.0 + 2.0 ** -8)).astype(np.float32)
+        k = synth.bf16_bits_from_f32(kf)
+        t = oracle.key_transform(k, 1, 1, center=1, mips=0)
+        assert t["status"] == 0
+        kx = synth.bf16_bits_to_f32(k).astype(np.float64)
+        c = t["c"].astype(np.float64)
+        assert np.max(np.abs(kx[[0, 11]]) / np.maximum(np.abs(c), 1e-300)) > 2.0 ** 29
+        for i in (0, 11):
+            for j in range(d):
+                exact = exact_ref.to_bf16(exact_ref.to_f32(Fraction(float(kx[i, j])) - Fraction(float(c[j]))))
+                got = float(synth.bf16_bits_to_f32(t["xbar"][i:i + 1, j:j + 1])[0, 0])
+                assert got == float(exact), (trial, i, j, got, float(exact))

@@ -1,0 +1,137 @@
+"""Estimator-quality harness: relative error of the attention output vs computation cost
+on synthetic decode workloads, for exact attention, TopK, oracle sampling and MagicPIG
+(Alg. 1) at several (K, L) -- the MagicPIG numbers both from the CPU oracle and from this library's CUDA path on
+the same inputs.  Cost = tokens whose K/V rows are read: m for TopK, |S| (unique draws) for oracle sampling,
+|S_g u T| for MagicPIG (the paper's Cost_2).  Writes one JSON document.
+
+  python tools/estimator_quality.py [--out profiles/r02_estimator_quality.json] [--n 8192] [--no-gpu]"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import synth  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="profiles/r02_estimator_quality.json")
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--units", type=int, default=2)
+    ap.add_argument("--no-gpu", action="store_true")
+    args = ap.parse_args()
+    bf = synth.bf16_bits_to_f32
+    gpu = None
+    if not args.no_gpu:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                import paper_2410_16179_b200 as pkg
+                gpu = (torch, pkg)
+        except Exception:
+            gpu = None
+    KL = [(8, 75), (9, 120), (10, 150), (11, 300)]
+    results = {"workload": None, "rows": []}
+    base = dataclasses.replace(synth.CONFIGS["C2"], n=args.n, B=1, Hq=4, Hkv=1)
+    results["workload"] = (f"synth C2-recipe units (b=0, kv heads 0..{args.units - 1}): n={args.n}, G=4, d=128, "
+                           f"planted {base.planted:.0%} keys at cos {base.planted_cos} with the group-mean query, "
+                           f"sink logit {base.sink_logit}, sink={base.sink}, local={base.local}")
+    rng = np.random.default_rng(20241021)
+    units = []
+    for h in range(args.units):
+        k, v, q = synth.make_unit(base, 0, h)
+        units.append(("iid-values", h, k, v, q))
+        # values with a component along one direction proportional to the key's (standardized) logit against
+        # the group-mean query: heavy tokens differ systematically from the tail, as in the zoo
+        kq = bf(k).astype(np.float64) @ bf(q).astype(np.float64).mean(0)
+        z = (kq - kq.mean()) / kq.std()
+        mu = np.random.default_rng(h).standard_normal(128)
+        v2 = synth.bf16_bits_from_f32((z[:, None] * mu[None, :] / 3 + bf(v)).astype(np.float32))
+        units.append(("logit-correlated-values", h, k, v2, q))
+    for wname, h, k, v, q in units:
+        kf, vf = bf(k).astype(np.float64), bf(v).astype(np.float64)
+        for g in range(base.G):
+            qf = bf(q[g]).astype(np.float64)
+            w = oracle.softmax_f64(kf @ qf / np.sqrt(128.0))
+            exact = oracle.expectation(w, vf)
+            row = {"values": wname, "unit": h, "head": g, "top20_mass": float(np.sort(w)[::-1][: args.n // 5].sum()), "topk": [],
+                   "oracle_sampling": [], "magicpig": []}
+            for frac in (0.005, 0.01, 0.02, 0.05):
+                m = max(1, int(frac * args.n))
+                row["topk"].append({"cost": m, "err": rel(oracle.topk_estimate(w, vf, m), exact)})
+            for B in (16, 64, 256, 1024):
+                errs, us = [], []
+                for _ in range(20):
+                    e, u = oracle.oracle_sampling(w, vf, rng.random(B))
+                    errs.append(rel(e, exact))
+                    us.append(u)
+                row["oracle_sampling"].append({"budget": B, "cost": float(np.mean(us)), "err": float(np.mean(errs)),
+                                               "expected_unique": oracle.expected_unique(w, B)})
+            results["rows"].append(row)
+        for K, L in KL:
+            W = synth.make_projections(K, L, base.mips)
+            ref = oracle.decode_unit(k, v, q, W, K, L, base.center, base.mips, base.min_collisions, base.sink,
+                                     base.local)
+            got = None
+            if gpu:
+                torch, pkg = gpu
+                dev = torch.device("cuda:0")
+                t = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
+                tk, tv, tq = t(k[None, None]), t(v[None, None]), t(q[None])
+                mp = pkg.MagicPIG(torch.from_numpy(W).to(dev), K=K, L=L).build(tk)
+                got = mp.decode(tq, tk, tv).cpu().numpy()[0]
+            for g in range(base.G):
+                qf = bf(q[g]).astype(np.float64)
+                w = oracle.softmax_f64(kf @ qf / np.sqrt(128.0))
+                exact = oracle.expectation(w, vf)
+                row = next(r for r in results["rows"] if r["unit"] == h and r["head"] == g and r["values"] == wname)
+                cost = int(np.count_nonzero(ref["in_s"][g]))
+                ent = {"K": K, "L": L, "cost": cost, "sampled": int(ref["s_count"][g]), "err_oracle": rel(ref["out"][g], exact)}
+                if got is not None:
+                    ent["err_gpu"] = rel(got[g].astype(np.float64), exact)
+                    ent["gpu_vs_oracle"] = rel(got[g].astype(np.float64), ref["out"][g])
+                row["magicpig"].append(ent)
+    # summary: mean error per method at comparable cost, per value model
+    summ = {}
+    for wname in ("iid-values", "logit-correlated-values"):
+        rows = [r for r in results["rows"] if r["values"] == wname]
+        sw = {}
+        for key in ("topk", "oracle_sampling"):
+            for i in range(len(rows[0][key])):
+                pts = [r[key][i] for r in rows]
+                sw[f"{key}[{i}]"] = {"cost": float(np.mean([p["cost"] for p in pts])),
+                                     "err": float(np.mean([p["err"] for p in pts]))}
+        for i, (K, L) in enumerate(KL):
+            pts = [r["magicpig"][i] for r in rows]
+            e = {"cost": float(np.mean([p["cost"] for p in pts])),
+                 "err_oracle": float(np.mean([p["err_oracle"] for p in pts]))}
+            if "err_gpu" in pts[0]:
+                e["err_gpu"] = float(np.mean([p["err_gpu"] for p in pts]))
+                e["gpu_vs_oracle_max"] = float(np.max([p["gpu_vs_oracle"] for p in pts]))
+            sw[f"magicpig(K={K},L={L})"] = e
+        summ[wname] = sw
+    results["summary"] = summ
+    results["note"] = ("err = ||estimate - exact|| / ||exact||, exact = fp64 softmax attention over all n keys; cost = "
+                       "tokens whose K/V rows are read; MagicPIG cost includes the static set T (sink + local)")
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(results, f, indent=1)
+    for wname, sw in summ.items():
+        print(wname)
+        for k_, v_ in sw.items():
+            print("  ", k_, {a: round(b, 4) for a, b in v_.items()})
+
+
+if __name__ == "__main__":
+    main()

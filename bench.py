@@ -69,15 +69,16 @@ def _peaks():
 
 def _traffic(kernel_key):
     """DRAM bytes per launch of a kernel (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
-    ncu --set full summary (tools/ncu_summary2.py), captured at the same workload, or None."""
+    ncu --set full summary (tools/ncu_summary2.py), captured at the same workload, as (bytes, source), or
+    None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         try:
             with open(p) as f:
                 d = json.load(f)
             e = d.get(kernel_key)
-            return {"bytes": e["dram_bytes_per_launch"], "source": f"profiles/ncu_summary.json ({d.get('tag')}, "
-                    f"{e.get('capture')})"} if e else None
+            return (e["dram_bytes_per_launch"], f"profiles/ncu_summary.json ({d.get('tag')}, "
+                    f"{e.get('capture')})") if e else None
         except Exception:
             return None
     return None
@@ -167,6 +168,19 @@ def _dist(expect_world):
             dist.init_process_group(backend)
         return dist, dist.get_rank(), ws
     return None, 0, 1
+
+
+def _dist_on():
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
+def _gather_parts(part, group=None):
+    """[P][rows][130] partial states of every rank (one rank: no collective)."""
+    if not _dist_on():
+        return part[None]
+    from paper_2410_16179_b200.sharding import all_gather_stacked
+    return all_gather_stacked(part, group)
 
 
 def _device(local_rank):
@@ -292,7 +306,7 @@ class Replicas:
             vr = tv if r == 0 else tv.clone()
             mp = pkg.MagicPIG(tW, K=wl.K, L=wl.L, center=wl.center, mips=wl.mips, min_collisions=wl.min_collisions,
                               sink=wl.sink, local=wl.local, buckets=(path == "buckets"))
-            if rw.mode == "sequence":
+            if rw.mode == "sequence" and _dist_on():
                 mp.build_sharded(kr, rw.seq_offset, wl.n, group)
             else:
                 mp.build(kr)
@@ -531,12 +545,10 @@ def run_ours(args):
 
         def full_step(i):
             graphs[i % R].replay()
-            allp = all_gather_stacked(part, group)
-            B_.merge_partials(allp, out_m)
+            B_.merge_partials(_gather_parts(part, group), out_m)
 
         def merge_only(i):
-            allp = all_gather_stacked(part, group)
-            B_.merge_partials(allp, out_m)
+            B_.merge_partials(_gather_parts(part, group), out_m)
         timed = full_step
     else:
         GS = min(args.steps, 64)
@@ -614,8 +626,10 @@ def run_ours(args):
         dom = max(m["kernels"], key=lambda kn: m["kernels"][kn]["us"])
         kd = m["kernels"][dom]
         kname = kd["kernel"].split(" ")[0]
+        tr = _traffic(kname)
         roof = {"bound": "hbm", "achieved": kd["GBs"], "peak": peaks["hbm"], "unit": "GB/s", "frac": kd["frac"],
-                "traffic": _traffic(kname), "kernel": kd["kernel"], "kernel_us": kd["us"],
+                "traffic": tr[0] if tr else None, "traffic_source": tr[1] if tr else None,
+                "kernel": kd["kernel"], "kernel_us": kd["us"],
                 "alg_bytes_per_launch": kd["alg_MB"] * 1e6, "peak_source": peak_src,
                 "step": {"alg_bytes": m["alg_bytes"]["step"], "us": m["step_us"], "GBs": m["step_GBs"],
                          "frac": m["step_frac"]}}
@@ -635,7 +649,7 @@ def run_ours(args):
             r = i % R
             qd.copy_(q_host, non_blocking=True)
             reps.mps[r].decode(qd, reps.ks[r], reps.vs[r], partial=part)
-            B_.merge_partials(all_gather_stacked(part, group), out_m)
+            B_.merge_partials(_gather_parts(part, group), out_m)
             out_host.copy_(out_m, non_blocking=True)
             torch.cuda.current_stream().synchronize()
     else:

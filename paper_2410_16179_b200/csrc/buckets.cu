@@ -125,10 +125,14 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_build_kernel(const uint32_t
 // loads of a run in flight before the shared-memory atomics.  Bucket sizes are very skewed (the query's
 // bucket can hold thousands of keys), so the split is over entries, not over tables.
 constexpr int BM_RUN = 8;
+// parts > 1 (grid.z = parts): CTA z handles the z-th slice of the head's flattened ids and writes its own
+// (seen once, seen twice) bitmaps, sbits[B][Hq][parts][2][nw]; the select step combines the parts with the
+// same saturating counter (P:84 rule).  Bucket sizes are skewed, so slicing by ids balances the CTAs.
 __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t* __restrict__ qbits,
                                                                   const int32_t* __restrict__ tables, int64_t Hq,
                                                                   int64_t Hkv, int64_t n_local, int K, int L, int KLw,
                                                                   int minc, uint32_t* __restrict__ sbits) {
+    const int parts = gridDim.z, part = blockIdx.z;
     asm volatile("griddepcontrol.launch_dependents;");  // the estimator kernel may start its prologue
     extern __shared__ uint32_t seen[];  // seen1[nw], seen2[nw], lo[L], start[L + 1]
     __shared__ int warp_tot[33];
@@ -161,7 +165,8 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
     if (tid == 0) start[L] = total;
     __syncthreads();
     const int32_t* ids0 = tu + (size_t)L * (nb + 1);
-    for (int e0 = tid * BM_RUN; e0 < total; e0 += blockDim.x * BM_RUN) {
+    const int e_beg = (int)((int64_t)total * part / parts), e_end = (int)((int64_t)total * (part + 1) / parts);
+    for (int e0 = e_beg + tid * BM_RUN; e0 < e_end; e0 += blockDim.x * BM_RUN) {
         int lo = 0, hi = L;  // table of flat index e0: last t with start[t] <= e0
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
         for (int j = 0; j < BM_RUN; j++) {
             const int e = e0 + j;
             ids[j] = -1;
-            if (e < total) {
+            if (e < e_end) {
                 while (e >= tnext) tnext = start[++t + 1];
                 ids[j] = __ldg(ids0 + (size_t)t * n_local + lo_s[t] + (e - start[t]));
             }
@@ -190,9 +195,14 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
         }
     }
     __syncthreads();
-    const uint32_t* src = minc > 1 ? seen2 : seen1;
-    uint32_t* dst = sbits + (b * Hq + hq) * nw;
-    for (int64_t w = tid; w < nw; w += blockDim.x) dst[w] = src[w];
+    if (parts == 1) {
+        const uint32_t* src = minc > 1 ? seen2 : seen1;
+        uint32_t* dst = sbits + (b * Hq + hq) * nw;
+        for (int64_t w = tid; w < nw; w += blockDim.x) dst[w] = src[w];
+    } else {
+        uint32_t* dst = sbits + ((b * Hq + hq) * parts + part) * 2 * nw;
+        for (int64_t w = tid; w < 2 * nw; w += blockDim.x) dst[w] = seen[w];
+    }
 }
 
 size_t bucket_tables_words(int K, int L, int64_t units, int64_t n_local) {
@@ -214,7 +224,7 @@ int launch_bucket_build(const uint32_t* codes, int64_t units, int64_t n_local, i
 }
 
 int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, int64_t Hq, int64_t Hkv,
-                       int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st) {
+                       int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st, int parts) {
     const size_t smem = (size_t)((n_local + 31) >> 5) * 8 + (size_t)(2 * L + 1) * 4;
     if (smem > 208 * 1024) return MAGICPIG_EINVAL;
     if (smem > 48 * 1024 &&
@@ -222,7 +232,7 @@ int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, 
             cudaSuccess)
         return MAGICPIG_ECUDA;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)Hq, (unsigned)B);
+    cfg.gridDim = dim3((unsigned)Hq, (unsigned)B, (unsigned)parts);
     cfg.blockDim = dim3(BM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;

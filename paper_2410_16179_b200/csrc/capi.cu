@@ -160,7 +160,7 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     const size_t parts5 = (size_t)(units + (int64_t)num_sms() * EST_WARPS) * G * PREC5 * 4;  // record u + warp
     w.parts = (float*)take(parts4 > parts5 ? parts4 : parts5);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
-    w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4);  // S bitmaps of the Query step
+    w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4 * 2 * BM_PARTS);  // Query step output
     w.ents = (uint32_t*)take((size_t)units * nch * KCHUNK * 4);  // v7 piece lists
     w.pcnt = (int32_t*)take((size_t)units * nch * 4);
     w.hpc = (int32_t*)take((size_t)B * Hq * nch * 4);
@@ -394,13 +394,14 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
         ea.out = out, ea.partial = partial, ea.s_count = s_count;
         ea.unit_ctr = w.unit_ctr, ea.parts = w.parts, ea.status = w.status, ea.urec = w.urec;
         ea.lutab = w.lutab;
+        ea.sparts = (v7 && tables) ? BM_PARTS : 1;
         const bool fused = v7 && !tables;  // the dense scan emits the piece lists itself
         // Query(HT, q_code) -> S bitmaps: bucketed tables or the dense code scan (PDL after the encode)
         int rc = 0;
         if (!(stages & 1)) {
         } else if (tables) {
             rc = launch_bucket_mark(w.qbits, tables, B, Hq, Hkv, n_local, cfg->K, cfg->L, g.KLw,
-                                    cfg->min_collisions, w.sbits, st);
+                                    cfg->min_collisions, w.sbits, st, v7 ? BM_PARTS : 1);
         } else {
             ScanArgs sa;
             memset(&sa, 0, sizeof(sa));

@@ -117,8 +117,32 @@ __global__ void __launch_bounds__(SEL_WPB * 32) select_kernel(EstArgs a) {
     const bool ok = wi < nwb;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // S bitmaps of the Query kernel
     uint32_t sg[G];
+    if (a.sparts <= 1) {
 #pragma unroll
-    for (int g = 0; g < G; g++) sg[g] = ok ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
+        for (int g = 0; g < G; g++) sg[g] = ok ? __ldcg(a.sbits + (qh0 + g) * nwb + wi) : 0u;
+    } else {
+        // combine the id slices' (seen once, seen twice) words: (a1, a2) + (b1, b2) = (a1|b1, a2|b2|(a1&b1))
+        const int P = a.sparts;
+        uint32_t w1[G][BM_PARTS], w2[G][BM_PARTS];
+#pragma unroll
+        for (int g = 0; g < G; g++)
+#pragma unroll
+            for (int p = 0; p < BM_PARTS; p++) {
+                const uint32_t* base = a.sbits + (((qh0 + g) * P + p) * 2) * nwb + wi;
+                w1[g][p] = (ok && p < P) ? __ldcg(base) : 0u;
+                w2[g][p] = (ok && p < P) ? __ldcg(base + nwb) : 0u;
+            }
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            uint32_t f1 = 0u, f2 = 0u;
+#pragma unroll
+            for (int p = 0; p < BM_PARTS; p++) {
+                f2 |= w2[g][p] | (f1 & w1[g][p]);
+                f1 |= w1[g][p];
+            }
+            sg[g] = a.minc > 1 ? f2 : f1;
+        }
+    }
     emit_piece<G>(a, sr, u, c, qh0, lane, sg);
 }
 __device__ __forceinline__ unsigned long long gtimer() {

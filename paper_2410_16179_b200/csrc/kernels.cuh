@@ -70,8 +70,14 @@ int launch_decode5(const DecodeArgs& a, int nsm, int max_smem, cudaStream_t st);
 size_t bucket_tables_words(int K, int L, int64_t units, int64_t n_local);
 int launch_bucket_build(const uint32_t* codes, int64_t units, int64_t n_local, int K, int L, int KLq,
                         int64_t nchunks, int32_t* tables, cudaStream_t st);
+#ifndef MP_BM_PARTS
+#define MP_BM_PARTS 1
+#endif
+constexpr int BM_PARTS = MP_BM_PARTS;  // id slices per (sequence, query head) in the v7 bucketed Query
+                                        // (A/B on B200: 1 = 84.8 us C3 step, 2 = 88.6, 4 = 91.9)
 int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, int64_t Hq, int64_t Hkv,
-                       int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st);
+                       int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st,
+                       int parts = 1);
 int decode5_halves(const DecodeArgs& a, int nsm);
 int launch_merge(const float* parts, int P, int64_t BH, float* out, cudaStream_t st);
 int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st);
@@ -118,7 +124,9 @@ struct EstArgs {
     const float* key_norm;
     const uint16_t* k;
     const uint16_t* v;
-    const uint32_t* sbits;        // [B][Hq][ceil(n/32)] S bitmaps of the Query step
+    const uint32_t* sbits;        // [B][Hq][ceil(n/32)] S bitmaps of the Query step, or with sparts > 1
+                                  // [B][Hq][sparts][2][ceil(n/32)] (seen once, seen twice) per id slice
+    int sparts;
     int64_t B, Hkv, Hq, n_local, seq_offset, n_global, nchunks;
     int K, L, minc, sink, local;
     int off_wbuf;                 // set by estimate_layout

@@ -417,7 +417,7 @@ def measure_decode(rw, path, dev, tW, peaks, k, v, q, graph_steps=64, group=None
                 ab["query"] += ab["select"]
             kern["estimate"] = {"us": _graph_time(stage(4), R, graph_steps), "note": "estimate + merge kernels"}
             names = {"query": "bucket_mark_kernel" if path == "buckets" else "scan6_kernel (select fused)",
-                     "select": "select_kernel", "estimate": "estimate_kernel" if choice == 7 else "estimate8_kernel"}
+                     "select": "select_kernel", "estimate": {7: "estimate_kernel", 8: "estimate8_kernel", 9: "estimate9_kernel"}[choice]}
             for nm in kern:
                 kern[nm]["alg_MB"] = ab[nm] / 1e6
         for nm, kd in kern.items():
@@ -508,6 +508,8 @@ def run_ours(args):
     from paper_2410_16179_b200 import binding as B_
 
     dist, rank, world = _dist(args.gpus)
+    if args.kernel:
+        B_.set_decode_kernel(args.kernel)
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     dev = _device(local_rank)
     torch.cuda.set_device(dev)
@@ -779,6 +781,7 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(MODES))
     ap.add_argument("--path", default="buckets", choices=["buckets", "dense"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", type=int, default=0, help="decode kernel (0 = the library's automatic choice)")
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-build", action="store_true")

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmagicpig.so")
-SOURCES = ["capi.cu", "build.cu", "hash_gemm.cu", "qencode.cu", "decode.cu", "decode5.cu", "codes_io.cu", "buckets.cu", "scan6.cu", "attend.cu", "estimate.cu", "estimate8.cu"]
+SOURCES = ["capi.cu", "build.cu", "hash_gemm.cu", "qencode.cu", "decode.cu", "decode5.cu", "codes_io.cu", "buckets.cu", "scan6.cu", "attend.cu", "estimate.cu", "estimate8.cu", "estimate9.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}"]

@@ -38,6 +38,8 @@ static int max_smem_optin() {
 // (5 for small decodes, else 7), 4..8 = a specific kernel generation (A/B arms); all compute the same S
 // bit for bit.
 static std::atomic<int> g_decode_kernel{0};
+// the auto choice for decodes larger than two chunk tiles per SM (A/B-selected on B200)
+constexpr int LARGE_KVER = 7;
 
 static bool cfg_ok(const magicpig_config* c) {
     if (!c) return false;
@@ -157,7 +159,7 @@ static DecodeWs decode_layout(const magicpig_config* c, int64_t B, int64_t Hq, i
     const int64_t nT = n_local < (int64_t)c->sink + c->local ? n_local : (int64_t)c->sink + c->local;
     const int64_t nst = nT > 0 ? (nT + KCHUNK - 1) / KCHUNK : 1;
     const size_t parts4 = (size_t)units * (nch + nst) * 8 * G * PART * 4;      // up to 8 CTAs per cluster
-    const size_t parts5 = (size_t)(units + (int64_t)num_sms() * EST_WARPS) * G * PREC5 * 4;  // record u + warp
+    const size_t parts5 = (size_t)(units + (int64_t)num_sms() * EST_MAX_WARPS) * G * PREC5 * 4;  // record u + warp
     w.parts = (float*)take(parts4 > parts5 ? parts4 : parts5);
     w.chunk_cnt = (int32_t*)take((size_t)units * nch * G * 4);
     w.sbits = (uint32_t*)take((size_t)B * Hq * ((n_local + 31) / 32) * 4 * 2 * BM_PARTS);  // Query step output
@@ -379,10 +381,11 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
         // select, the balanced estimator, the unit merge), which scales with the sampled rows
         DecodeArgs t = a;
         const bool small = B * Hkv * g.nchunks <= 2 * (int64_t)num_sms() && decode5_layout(t, (int)G, max_smem_optin());
-        kver = small ? 5 : 7;
+        kver = small ? 5 : LARGE_KVER;
     }
-    if ((kver % 10 == 6 && !timeline) || kver % 10 == 7 || kver % 10 == 8) {
-        const bool v7 = (kver % 10 == 7 || kver % 10 == 8) && B * Hkv * (g.nchunks + 1) <= EST_MAX_PIECES &&
+    if (kver % 10 == 9 && timeline) kver = 7;  // kernel 9 keeps no timeline
+    if ((kver % 10 == 6 && !timeline) || kver % 10 == 7 || kver % 10 == 8 || kver % 10 == 9) {
+        const bool v7 = (kver % 10 == 7 || kver % 10 == 8 || kver % 10 == 9) && B * Hkv * (g.nchunks + 1) <= EST_MAX_PIECES &&
                         n_local < (1 << 24);
         EstArgs ea;
         memset(&ea, 0, sizeof(ea));
@@ -431,6 +434,8 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
             if (kver % 10 == 8 && estimate8_ok(ea, max_smem_optin())) {
                 if (grid_out) *grid_out = num_sms();  // timeline rows (one per CTA)
                 rc = launch_estimate8(ea, num_sms(), max_smem_optin(), st);
+            } else if (kver % 10 == 9) {
+                rc = launch_estimate9(ea, num_sms(), max_smem_optin(), st);
             } else {
                 rc = launch_estimate(ea, num_sms(), max_smem_optin(), st);
             }
@@ -486,14 +491,14 @@ extern "C" int magicpig_debug_decode_kernel_choice(const magicpig_config* cfg, i
         t.K = cfg->K, t.L = cfg->L, t.KL = g.KL, t.KLw = g.KLw, t.KLq = g.KLq, t.ngroups = g.ngroups;
         t.TG = g.TG, t.QG = g.QG, t.nchunks = g.nchunks, t.B = B, t.Hkv = Hkv, t.Hq = Hq, t.n_local = n_local;
         const bool small = B * Hkv * g.nchunks <= 2 * (int64_t)num_sms() && decode5_layout(t, (int)G, max_smem_optin());
-        kver = small ? 5 : 7;
+        kver = small ? 5 : LARGE_KVER;
     }
     (void)buckets;
     return kver % 10;
 }
 
 extern "C" int magicpig_debug_set_decode_kernel(int version) {
-    if (version != 0 && (version % 10 < 4 || version % 10 > 8)) return MAGICPIG_EINVAL;
+    if (version != 0 && (version % 10 < 4 || version % 10 > 9)) return MAGICPIG_EINVAL;
     g_decode_kernel.store(version);
     return MAGICPIG_OK;
 }
@@ -602,7 +607,7 @@ int magicpig_debug_decode_sets(const magicpig_config* cfg, const uint16_t* q, in
     if (rc) return rc;
     return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, seq_offset, n_global, out,
                        nullptr, nullptr, s_mask, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, weighted, 7,
-                       kv == 0 ? 7 : kv);
+                       kv == 0 ? LARGE_KVER : kv);
 }
 
 int magicpig_decode_host(const magicpig_config* cfg, const uint16_t* q_host, int64_t Hq, const uint32_t* codes,
@@ -636,7 +641,7 @@ int magicpig_debug_decode_stage(const magicpig_config* cfg, int stage, const uin
     const int kv = g_decode_kernel.load();
     if ((kv != 0 && kv % 10 < 6) || n_local < 1) return MAGICPIG_EINVAL;
     return decode_impl(cfg, q, Hq, codes, center, key_norm, k, v, B, Hkv, n_local, 0, n_local, out, nullptr, nullptr,
-                       nullptr, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, nullptr, stage, kv == 0 ? 7 : kv);
+                       nullptr, ws, ws_bytes, stream, nullptr, 0, nullptr, tables, nullptr, stage, kv == 0 ? LARGE_KVER : kv);
 }
 
 int magicpig_debug_build_phases(const magicpig_config* cfg, const uint16_t* k, int64_t B, int64_t Hkv, int64_t n,

@@ -149,6 +149,11 @@ struct EstArgs {
 #define MP_EST_WARPS 8
 #endif
 constexpr int EST_WARPS = MP_EST_WARPS;  // warps per estimator CTA
+#ifndef MP_EST9_WARPS
+#define MP_EST9_WARPS 12
+#endif
+constexpr int EST9_WARPS = MP_EST9_WARPS;  // warps per kernel-9 estimator CTA
+constexpr int EST_MAX_WARPS = EST_WARPS > EST9_WARPS ? EST_WARPS : EST9_WARPS;
 constexpr int EST_MAX_PIECES = 12288;  // units * (chunks + 1): the estimator's piece prefix in smem
 int launch_select(const EstArgs& a, cudaStream_t st);
 size_t estimate_layout(EstArgs& a, int G);
@@ -156,6 +161,7 @@ int launch_estimate(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
 int launch_est_merge(const EstArgs& a, cudaStream_t st);
 bool estimate8_ok(const EstArgs& a, int max_smem);
 int launch_estimate8(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
+int launch_estimate9(const EstArgs& a, int nsm, int max_smem, cudaStream_t st);
 
 // ---- decode v6: Query (dense scan6 or bucketed bucket_mark) -> S bitmaps -> estimator (attend)
 struct ScanArgs {

@@ -22,7 +22,7 @@ def _bf(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to("cuda:0")
 
 
-@pytest.mark.parametrize("buckets,kernel", [(False, 0), (True, 0), (False, 7), (False, 8)])
+@pytest.mark.parametrize("buckets,kernel", [(False, 0), (True, 0), (False, 7), (False, 8), (True, 9)])
 def test_append_decode_loop(buckets, kernel):
     import paper_2410_16179_b200 as pkg
     steps, n0 = 20, 2040

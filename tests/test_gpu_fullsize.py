@@ -71,7 +71,7 @@ def _check(wl, out, s_count, s_mask, refs, units, n):
             assert _rel_err(out[b, row], ref["out"][g]) <= TOL, (b, row)
 
 
-@pytest.mark.parametrize("name,kernel,buckets", [("C3", 0, True), ("C3", 0, False), ("C3", 8, True), ("C4", 0, False)])
+@pytest.mark.parametrize("name,kernel,buckets", [("C3", 0, True), ("C3", 0, False), ("C3", 8, True), ("C3", 9, True), ("C4", 9, False), ("C4", 0, False)])
 def test_baseline_config_sampled_units(name, kernel, buckets):
     pkg = _pkg()
     wl = synth.CONFIGS[name]

@@ -20,9 +20,10 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-3
 
 
-@pytest.fixture(params=[8, 7, 6, 5], ids=["k8", "k7", "k6", "k5"], autouse=True)
+@pytest.fixture(params=[9, 8, 7, 6, 5], ids=["k9", "k8", "k7", "k6", "k5"], autouse=True)
 def decode_kernel(request):
-    """Every parity test runs on four decode paths: 8 = Query kernel + select (per-piece S_g u T
+    """Every parity test runs on five decode paths: 9 = kernel 7's pipeline with the K/V rows gathered
+    by plain 16-B loads straight into the mma fragments (no shared-memory staging), 8 = Query kernel + select (per-piece S_g u T
     lists) + the tcgen05 estimator (TMA gather4 tiles, TMEM accumulators), 7 = the same with the
     mma.sync estimator (every warp a contiguous range), 6 = Query kernel + estimator kernel with a
     producer warp, and 5 = the persistent fused kernel (which falls back to the cluster-per-chunk

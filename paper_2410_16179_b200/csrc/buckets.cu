@@ -15,10 +15,13 @@
 //                        by the decode kernel in place of the code scan.
 // S is the same set as the dense scan computes (oracle pin P10 proves the two
 // forms equal in the oracle; the GPU parity tests check both against it).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace mp {
+namespace cgr = cooperative_groups;
 
 constexpr int BK_THREADS = 512;
 constexpr int BM_THREADS = 512;
@@ -205,6 +208,195 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
     }
 }
 
+// v2 (parts == 1): the same S, with the L bucket ranges cut into 32-id chunks (prefix over the chunk counts)
+// and the chunks dealt to the warps, BM2_UNROLL chunks per warp in flight: one coalesced 128-B load per
+// chunk, the chunk's table found once per round (binary search, then a forward walk), no per-id address
+// search.  1024 threads per CTA: the heaviest query head (about twice the mean, C3) sets the kernel time.
+constexpr int BM2_THREADS = 1024;
+constexpr int BM2_UNROLL = 4;
+__global__ void __launch_bounds__(BM2_THREADS) bucket_mark2_kernel(const uint32_t* __restrict__ qbits,
+                                                                    const int32_t* __restrict__ tables, int64_t Hq,
+                                                                    int64_t Hkv, int64_t n_local, int K, int L,
+                                                                    int KLw, int minc, uint32_t* __restrict__ sbits) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    extern __shared__ uint32_t seen[];  // seen1[nw], seen2[nw], lo[L], len[L], cstart[L + 1]
+    __shared__ int warp_tot[33];
+    const int64_t hq = blockIdx.x, b = blockIdx.y;
+    const int64_t G = Hq / Hkv, u = b * Hkv + hq / G;
+    const int nb = 1 << K;
+    const int nw = (int)((n_local + 31) >> 5);
+    uint32_t* seen1 = seen;
+    uint32_t* seen2 = seen + nw;
+    int* lo_s = reinterpret_cast<int*>(seen + 2 * nw);
+    int* len_s = lo_s + L;
+    int* cstart = len_s + L;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    for (int w = tid; w < 2 * nw; w += BM2_THREADS) seen[w] = 0u;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
+    const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
+    for (int t = tid; t < L; t += BM2_THREADS) {
+        const int c0 = t * K;  // query code of table t: columns t*K .. t*K+K-1 (little endian, R7)
+        const uint64_t two = (uint64_t)__ldcg(qb + (c0 >> 5)) |
+                             ((c0 >> 5) + 1 < KLw ? (uint64_t)__ldcg(qb + (c0 >> 5) + 1) << 32 : 0ull);
+        const int qc = (int)((two >> (c0 & 31)) & (uint64_t)(nb - 1));
+        const int32_t* offs = tu + (size_t)t * (nb + 1);
+        const int lo = __ldg(offs + qc), hi = __ldg(offs + qc + 1);
+        lo_s[t] = lo;
+        len_s[t] = hi - lo;
+        cstart[t] = (hi - lo + 31) >> 5;
+    }
+    __syncthreads();
+    const int C = block_exclusive_scan(cstart, L, warp_tot);  // cstart[t] = first chunk of table t
+    if (tid == 0) cstart[L] = C;
+    __syncthreads();
+    const int32_t* ids0 = tu + (size_t)L * (nb + 1);
+    constexpr int NWP = BM2_THREADS / 32;
+    for (int c0 = warp * BM2_UNROLL; c0 < C; c0 += NWP * BM2_UNROLL) {
+        int lo = 0, hi = L;  // table of chunk c0: last t with cstart[t] <= c0 (warp-uniform)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cstart[mid] <= c0) lo = mid;
+            else hi = mid;
+        }
+        int t = lo;
+        int ids[BM2_UNROLL];
+#pragma unroll
+        for (int j = 0; j < BM2_UNROLL; j++) {
+            const int c = c0 + j;
+            ids[j] = -1;
+            if (c < C) {
+                while (c >= cstart[t + 1]) t++;
+                const int off = ((c - cstart[t]) << 5) + lane;
+                if (off < len_s[t]) ids[j] = __ldg(ids0 + (size_t)t * n_local + lo_s[t] + off);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < BM2_UNROLL; j++) {
+            if (ids[j] >= 0) {
+                const int i = ids[j];
+                const uint32_t bit = 1u << (i & 31);
+                const uint32_t old = atomicOr(&seen1[i >> 5], bit);
+                if (minc > 1 && (old & bit)) atomicOr(&seen2[i >> 5], bit);
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t* src = minc > 1 ? seen2 : seen1;
+    uint32_t* dst = sbits + (b * Hq + hq) * nw;
+    for (int w = tid; w < nw; w += BM2_THREADS) dst[w] = src[w];
+}
+
+// v3 (parts == 1, the default): a cluster of BM3_CS CTAs per (sequence, query head).  The head's bucket ranges
+// are cut into 32-id chunks; CTA r of the cluster takes the r-th contiguous share of the chunks, warp w of the
+// CTA the w-th contiguous share of that (one binary search per warp, then a forward walk over the tables),
+// BM3_UNROLL chunks (one coalesced 128-B load each) in flight per warp.  Each CTA marks its own seen-once /
+// seen-twice bitmaps; after a cluster barrier CTA 0 combines them through distributed shared memory with the
+// same saturating counter, (a1, a2) + (b1, b2) = (a1 | b1, a2 | b2 | (a1 & b1)), and writes S.  Splitting a
+// head over two SMs halves the heaviest head's time (the C3 heads' id counts are skewed: max ~1.9x the mean).
+constexpr int BM3_THREADS = 512;
+constexpr int BM3_UNROLL = 4;
+#ifndef MP_BM3_CS
+#define MP_BM3_CS 2
+#endif
+constexpr int BM3_CS = MP_BM3_CS;
+__global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_t* __restrict__ qbits,
+                                                                    const int32_t* __restrict__ tables, int64_t Hq,
+                                                                    int64_t Hkv, int64_t n_local, int K, int L,
+                                                                    int KLw, int minc, uint32_t* __restrict__ sbits) {
+    #ifndef MP_BM3_LD_END
+#define MP_BM3_LD_END 1
+#endif
+    if (!MP_BM3_LD_END) asm volatile("griddepcontrol.launch_dependents;");
+    extern __shared__ uint32_t seen[];  // seen1[nw], seen2[nw], base[L], len[L], cstart[L + 1]
+    __shared__ int warp_tot[33];
+    cgr::cluster_group cluster = cgr::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int64_t hq = blockIdx.x / BM3_CS, b = blockIdx.y;
+    const int64_t G = Hq / Hkv, u = b * Hkv + hq / G;
+    const int nb = 1 << K;
+    const int nw = (int)((n_local + 31) >> 5);
+    uint32_t* seen1 = seen;
+    uint32_t* seen2 = seen + nw;
+    int* base_s = reinterpret_cast<int*>(seen + 2 * nw);
+    int* len_s = base_s + L;
+    int* cstart = len_s + L;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    for (int w = tid; w < 2 * nw; w += BM3_THREADS) seen[w] = 0u;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
+    const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
+    for (int t = tid; t < L; t += BM3_THREADS) {
+        const int c0 = t * K;  // query code of table t: columns t*K .. t*K+K-1 (little endian, R7)
+        const uint64_t two = (uint64_t)__ldcg(qb + (c0 >> 5)) |
+                             ((c0 >> 5) + 1 < KLw ? (uint64_t)__ldcg(qb + (c0 >> 5) + 1) << 32 : 0ull);
+        const int qc = (int)((two >> (c0 & 31)) & (uint64_t)(nb - 1));
+        const int32_t* offs = tu + (size_t)t * (nb + 1);
+        const int lo = __ldg(offs + qc), hi = __ldg(offs + qc + 1);
+        base_s[t] = (int)((int64_t)t * n_local + lo);  // < L * n_local (checked on the host)
+        len_s[t] = hi - lo;
+        cstart[t] = (hi - lo + 31) >> 5;
+    }
+    __syncthreads();
+    const int C = block_exclusive_scan(cstart, L, warp_tot);  // cstart[t] = first chunk of table t
+    if (tid == 0) cstart[L] = C;
+    __syncthreads();
+    const int32_t* ids0 = tu + (size_t)L * (nb + 1);
+    constexpr int NWP = BM3_THREADS / 32;
+    const int cr0 = (int)((int64_t)C * rank / BM3_CS), cr1 = (int)((int64_t)C * (rank + 1) / BM3_CS);
+    const int cw0 = cr0 + (int)((int64_t)(cr1 - cr0) * warp / NWP);
+    const int cw1 = cr0 + (int)((int64_t)(cr1 - cr0) * (warp + 1) / NWP);
+    int t = 0;
+    if (cw0 < cw1) {  // table of chunk cw0: last t with cstart[t] <= cw0
+        int lo = 0, hi = L;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cstart[mid] <= cw0) lo = mid;
+            else hi = mid;
+        }
+        t = lo;
+    }
+    for (int c0 = cw0; c0 < cw1; c0 += BM3_UNROLL) {
+        int ids[BM3_UNROLL];
+#pragma unroll
+        for (int j = 0; j < BM3_UNROLL; j++) {
+            const int c = c0 + j;
+            ids[j] = -1;
+            if (c < cw1) {
+                while (c >= cstart[t + 1]) t++;
+                const int off = ((c - cstart[t]) << 5) + lane;
+                if (off < len_s[t]) ids[j] = __ldg(ids0 + base_s[t] + off);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < BM3_UNROLL; j++) {
+            if (ids[j] >= 0) {
+                const int i = ids[j];
+                const uint32_t bit = 1u << (i & 31);
+                const uint32_t old = atomicOr(&seen1[i >> 5], bit);
+                if (minc > 1 && (old & bit)) atomicOr(&seen2[i >> 5], bit);
+            }
+        }
+    }
+    cluster.sync();  // every CTA's bitmaps complete
+    if (rank == 0) {
+        uint32_t* dst = sbits + (b * Hq + hq) * nw;
+        for (int w = tid; w < nw; w += BM3_THREADS) {
+            uint32_t f1 = seen1[w], f2 = seen2[w];
+#pragma unroll
+            for (int r = 1; r < BM3_CS; r++) {
+                const uint32_t* rs = cluster.map_shared_rank(seen, r);
+                const uint32_t b1 = rs[w], b2 = rs[nw + w];
+                f2 |= b2 | (f1 & b1);
+                f1 |= b1;
+            }
+            dst[w] = minc > 1 ? f2 : f1;
+        }
+    }
+    cluster.sync();  // the other CTAs' shared memory stays alive until CTA 0 has read it
+    if (MP_BM3_LD_END) asm volatile("griddepcontrol.launch_dependents;");
+}
+
 size_t bucket_tables_words(int K, int L, int64_t units, int64_t n_local) {
     return (size_t)units * L * (((size_t)1 << K) + 1 + (size_t)n_local);
 }
@@ -223,8 +415,61 @@ int launch_bucket_build(const uint32_t* codes, int64_t units, int64_t n_local, i
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
+#ifndef MP_BM2
+#define MP_BM2 3
+#endif
 int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, int64_t Hq, int64_t Hkv,
                        int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st, int parts) {
+    if (MP_BM2 == 3 && parts == 1 && (int64_t)L * n_local < (1ll << 31)) {
+        const size_t smem3 = (size_t)((n_local + 31) >> 5) * 8 + (size_t)(3 * L + 1) * 4;
+        if (smem3 <= 208 * 1024) {
+            if (smem3 > 48 * 1024 && cudaFuncSetAttribute(bucket_mark3_kernel,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          (int)smem3) != cudaSuccess)
+                return MAGICPIG_ECUDA;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(Hq * BM3_CS), (unsigned)B, 1u);
+            cfg.blockDim = dim3(BM3_THREADS);
+            cfg.dynamicSmemBytes = smem3;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            attr[1].id = cudaLaunchAttributeClusterDimension;
+            attr[1].val.clusterDim.x = BM3_CS;
+            attr[1].val.clusterDim.y = 1;
+            attr[1].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 2;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, bucket_mark3_kernel, qbits, tables, Hq, Hkv, n_local, K, L, KLw,
+                                               minc, sbits);
+            count_launch(1);
+            return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+        }
+    }
+    if (MP_BM2 == 2 && parts == 1) {
+        const size_t smem2 = (size_t)((n_local + 31) >> 5) * 8 + (size_t)(3 * L + 1) * 4;
+        if (smem2 <= 208 * 1024) {
+            if (smem2 > 48 * 1024 && cudaFuncSetAttribute(bucket_mark2_kernel,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          (int)smem2) != cudaSuccess)
+                return MAGICPIG_ECUDA;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)Hq, (unsigned)B, 1u);
+            cfg.blockDim = dim3(BM2_THREADS);
+            cfg.dynamicSmemBytes = smem2;
+            cfg.stream = st;
+            cudaLaunchAttribute attr;
+            attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr.val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = &attr;
+            cfg.numAttrs = 1;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, bucket_mark2_kernel, qbits, tables, Hq, Hkv, n_local, K, L, KLw,
+                                               minc, sbits);
+            count_launch(1);
+            return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+        }
+    }
     const size_t smem = (size_t)((n_local + 31) >> 5) * 8 + (size_t)(2 * L + 1) * 4;
     if (smem > 208 * 1024) return MAGICPIG_EINVAL;
     if (smem > 48 * 1024 &&

@@ -39,7 +39,7 @@ static int max_smem_optin() {
 // bit for bit.
 static std::atomic<int> g_decode_kernel{0};
 // the auto choice for decodes larger than two chunk tiles per SM (A/B-selected on B200)
-constexpr int LARGE_KVER = 7;
+constexpr int LARGE_KVER = 9;
 
 static bool cfg_ok(const magicpig_config* c) {
     if (!c) return false;

@@ -100,7 +100,10 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
             const bool live = j0 + col < KL && h < BHq;
             const float s = acc[nt][e];
             int bit = s > 0.0f;
-            if (live && !(fabsf(s) > 0x1p-16f * bnd[nt][e])) {
+#ifndef MP_QE_CERT
+#define MP_QE_CERT 0x1p-16f
+#endif
+            if (live && !(fabsf(s) > MP_QE_CERT * bnd[nt][e])) {
                 // rare: this thread recomputes the dot in fp64, then exactly
                 double sd = 0.0, bd = 0.0;
                 for (int d = 0; d < HD; d++) {
@@ -134,7 +137,10 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
         if (hb < BHq) qbits[hb * KLw + (j0 >> 5)] = wb;
     }
     __shared__ int lut_todo;
-    if (lutab) {  // after the codes: off the Query kernel's critical path until this grid completes
+#ifndef MP_QE_LUTCHK
+#define MP_QE_LUTCHK 1
+#endif
+    if (lutab && (MP_QE_LUTCHK || (blockIdx.x == 0 && blockIdx.y == 0))) {  // after the codes: off the Query kernel's critical path until this grid completes
         // the estimator's ln u(p) table (Eq.) in fp64, spread over the CTAs; kept in the workspace
         // and refilled only when (K, L, min_collisions) change: header word = key, next word = arrivals
         uint32_t* hdr = reinterpret_cast<uint32_t*>(lutab + LUT_N + 2);

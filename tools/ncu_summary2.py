@@ -73,16 +73,24 @@ def short(name):
 
 def main():
     tag, reps = sys.argv[1], sys.argv[2:]
-    out = {"tag": tag, "source": "ncu --set full --clock-control none (one launch per kernel, cold caches)"}
+    path = os.path.join("profiles", "ncu_summary.json")
+    out = {}
+    if os.path.exists(path):  # entries of earlier captures are kept (each names its own tag and capture)
+        with open(path) as f:
+            out = json.load(f)
+        for k, v in out.items():
+            if isinstance(v, dict) and "tag" not in v:
+                v["tag"] = out.get("tag")
+    out.update({"tag": tag, "source": "ncu --set full --clock-control none (one launch per kernel, cold caches)"})
     for rep in reps:
         s = summarize(rep)
         if s:
             s["capture"] = os.path.basename(rep)
+            s["tag"] = tag
             out[short(s["kernel"])] = s
             print(short(s["kernel"]), {k: (round(v, 3) if isinstance(v, float) else v) for k, v in s.items()
                                          if k in ("duration_ns", "dram_bytes_per_launch", "dram_pct", "sm_pct",
                                                   "tensor_pct", "issue_pct", "top_stalls")})
-    path = os.path.join("profiles", "ncu_summary.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", path)

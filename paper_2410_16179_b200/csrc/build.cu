@@ -16,6 +16,23 @@ __device__ __forceinline__ bool is_static_pos(int64_t pos, int64_t n_global, int
     return pos < (int64_t)sink || pos >= n_global - (int64_t)local;
 }
 
+// q64 accumulation of bf16 values in two int64 words, total = hi * 2^40 + lo: the same integers as summing
+// q64_of_bf16 (value * 2^64 = M * 2^s, s = e - 70, truncated toward zero for s < 0), without 128-bit shifts.
+// |k| < 2^27 gives s <= 83, so a term is < 2^52 in hi (s >= 40) or < 2^48 in lo; a lane adds at most
+// STATS_SPLIT / 8 = 128 terms per split, so neither word can overflow.
+__device__ __forceinline__ void q64_acc_bf16(long long& hi, long long& lo, uint16_t h) {
+    const int E = (h >> 7) & 0xFF;
+    const long long M = (long long)((h & 0x7Fu) | (E ? 0x80u : 0u));
+    const int s = (E ? E : 1) - 70;
+    long long vhi = 0, vlo = 0;
+    if (s >= 40) vhi = M << (s - 40);
+    else if (s >= 0) vlo = M << s;
+    else if (s > -8) vlo = M >> (-s);
+    if (h & 0x8000u) vhi = -vhi, vlo = -vlo;
+    hi += vhi;
+    lo += vlo;
+}
+
 // ---------------------------------------------------------------------------
 // Phase 1: per (unit, split, dim) partial sums of q64(k) over dynamic keys.
 // grid (nsplit, units), block 256: warp per key (stride 8), lane = 4 dims,
@@ -29,27 +46,38 @@ __global__ void __launch_bounds__(256) key_stats_partial_kernel(
     const int64_t i0 = (int64_t)split * STATS_SPLIT;
     const int64_t i1 = min(i0 + (int64_t)STATS_SPLIT, n_local);
     const uint16_t* kp = k + unit * n_local * HD;
-    i128 acc[4] = {0, 0, 0, 0};
+    long long ahi[4] = {0, 0, 0, 0}, alo[4] = {0, 0, 0, 0};
     int cnt = 0;
     bool bad = false;
-    for (int64_t i = i0 + warp; i < i1; i += 8) {
-        if (is_static_pos(seq_offset + i, n_global, sink, local)) continue;
-        const uint2 kr = __ldg(reinterpret_cast<const uint2*>(kp + i * HD) + lane);
-        const uint16_t h[4] = {(uint16_t)(kr.x & 0xFFFF), (uint16_t)(kr.x >> 16), (uint16_t)(kr.y & 0xFFFF),
-                               (uint16_t)(kr.y >> 16)};
+    constexpr int UN = 4;  // keys in flight per warp (all loads issued before the accumulation)
+    for (int64_t i = i0 + warp; i < i1; i += 8 * UN) {
+        uint2 kr[UN];
+        bool ok[UN];
 #pragma unroll
-        for (int t = 0; t < 4; t++) {
-            bad |= fabsf(bf2f(h[t])) >= ABS_LIMIT;
-            acc[t] += q64_of_bf16(h[t]);
+        for (int u = 0; u < UN; u++) {
+            const int64_t ii = i + 8 * u;
+            ok[u] = ii < i1 && !is_static_pos(seq_offset + ii, n_global, sink, local);
+            kr[u] = ok[u] ? __ldg(reinterpret_cast<const uint2*>(kp + ii * HD) + lane) : make_uint2(0u, 0u);
         }
-        cnt++;
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+            if (!ok[u]) continue;
+            const uint16_t h[4] = {(uint16_t)(kr[u].x & 0xFFFF), (uint16_t)(kr[u].x >> 16),
+                                   (uint16_t)(kr[u].y & 0xFFFF), (uint16_t)(kr[u].y >> 16)};
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                bad |= fabsf(bf2f(h[t])) >= ABS_LIMIT;
+                q64_acc_bf16(ahi[t], alo[t], h[t]);
+            }
+            cnt++;
+        }
     }
     if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
     __shared__ unsigned long long sm[8][HD][2];
     __shared__ int scnt[8];
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-        const u128 u = (u128)acc[t];
+        const u128 u = (u128)(((i128)ahi[t] << 40) + (i128)alo[t]);
         sm[warp][lane * 4 + t][0] = (unsigned long long)u;
         sm[warp][lane * 4 + t][1] = (unsigned long long)(u >> 64);
     }
@@ -171,12 +199,23 @@ __global__ void __launch_bounds__(256) r2_partial_kernel(const uint16_t* __restr
     const uint16_t* kp = k + unit * n_local * HD;
     u128 best = 0;
     bool bad = false;
-    for (int64_t i = i0 + warp; i < i1; i += 8) {
-        if (is_static_pos(seq_offset + i, n_global, sink, local)) continue;
-        uint2 kr = reinterpret_cast<const uint2*>(kp + i * HD)[lane];
-        uint32_t a, b;
-        u128 s = warp_sum_u128(transform4(kr, c, a, b, bad));
-        best = s > best ? s : best;
+    constexpr int UN = 4;  // keys in flight per warp
+    for (int64_t i = i0 + warp; i < i1; i += 8 * UN) {
+        uint2 kr[UN];
+        bool ok[UN];
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+            const int64_t ii = i + 8 * u;
+            ok[u] = ii < i1 && !is_static_pos(seq_offset + ii, n_global, sink, local);
+            kr[u] = ok[u] ? __ldg(reinterpret_cast<const uint2*>(kp + ii * HD) + lane) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+            if (!ok[u]) continue;  // warp-uniform
+            uint32_t a, b;
+            u128 s = warp_sum_u128(transform4(kr[u], c, a, b, bad));
+            best = s > best ? s : best;
+        }
     }
     if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
     __shared__ unsigned long long sm[8][2];
@@ -192,6 +231,148 @@ __global__ void __launch_bounds__(256) r2_partial_kernel(const uint16_t* __restr
             m = v > m ? v : m;
         }
         st_q64(part_r2 + (unit * nsplit + split) * 2, (i128)m);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Lane-per-key forms of phases 2b and 3a (the same integers as the warp-per-key forms above, without the
+// per-key 128-bit warp reductions): a thread reads its key's whole row (16 x 16 B), forms
+// x = bf16(fl32(k - c)) element by element, and sums q64(x^2) exactly in three int64 words.
+// x = +-m 2^(Ex - 134) (m <= 255 incl. the implicit bit) -> q64(x^2) = trunc(m^2 2^s), s = 2 Ex - 204 (the
+// fp32 square of a bf16 value is exact, and q64_of_f32 truncates the same product); |x| < 2^27 gives
+// s <= 102.  Words: hi (scale 2^64, s >= 64), mid (2^32, 32 <= s < 64), lo (s < 32); every term is below
+// 2^54 and a row adds 128 of them, so no word overflows.
+struct N2Acc {
+    unsigned long long hi, mid, lo;
+};
+__device__ __forceinline__ void n2_add(N2Acc& a, uint16_t xb) {
+    const int E = (xb >> 7) & 0xFF;
+    const unsigned long long m = (xb & 0x7Fu) | (E ? 0x80u : 0u);
+    const unsigned long long m2 = m * m;
+    const int sx = 2 * (E ? E : 1) - 204;
+    if (sx >= 64) a.hi += m2 << (sx - 64);
+    else if (sx >= 32) a.mid += m2 << (sx - 32);
+    else if (sx >= 0) a.lo += m2 << sx;
+    else if (sx > -16) a.lo += m2 >> (-sx);
+}
+__device__ __forceinline__ u128 n2_total(const N2Acc& a) {
+    return ((u128)a.hi << 64) + ((u128)a.mid << 32) + (u128)a.lo;
+}
+// one key row: x pairs (xw[w] = bf16 pair of dims 2w, 2w+1) and the exact q64 |x|^2; c from shared memory
+__device__ __forceinline__ u128 row_xbar(const uint16_t* __restrict__ krow, const float* __restrict__ cs,
+                                         uint32_t (&xw)[64], bool& bad) {
+    N2Acc acc = {0ull, 0ull, 0ull};
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        const uint4 kv = __ldg(reinterpret_cast<const uint4*>(krow) + q);
+        const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int d = 8 * q + 2 * t;
+            const uint16_t b0 = f2bf_rn(__fsub_rn(__uint_as_float(kk[t] << 16), cs[d]));
+            const uint16_t b1 = f2bf_rn(__fsub_rn(__uint_as_float(kk[t] & 0xFFFF0000u), cs[d + 1]));
+            bad |= fabsf(bf2f(b0)) >= ABS_LIMIT || fabsf(bf2f(b1)) >= ABS_LIMIT;
+            n2_add(acc, b0);
+            n2_add(acc, b1);
+            xw[4 * q + t] = (uint32_t)b0 | ((uint32_t)b1 << 16);
+        }
+    }
+    return n2_total(acc);
+}
+
+// Phase 2b, lane per key: grid (nsplit, units), block 256; thread t of split s takes keys s*1024 + t + 256 j
+__global__ void __launch_bounds__(256) r2_partial2_kernel(const uint16_t* __restrict__ k, int64_t n_local,
+                                                          int64_t seq_offset, int64_t n_global, int sink,
+                                                          int local, const float* __restrict__ center,
+                                                          int64_t* __restrict__ part_r2, uint32_t* status) {
+    __shared__ float cs[HD];
+    __shared__ unsigned long long sm[8][2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t unit = blockIdx.y;
+    const int split = blockIdx.x, nsplit = gridDim.x;
+    if (tid < HD) cs[tid] = center[unit * HD + tid];
+    __syncthreads();
+    const int64_t i0 = (int64_t)split * STATS_SPLIT;
+    const int64_t i1 = min(i0 + (int64_t)STATS_SPLIT, n_local);
+    const uint16_t* kp = k + unit * n_local * HD;
+    u128 best = 0;
+    bool bad = false;
+    for (int64_t i = i0 + tid; i < i1; i += 256) {
+        if (is_static_pos(seq_offset + i, n_global, sink, local)) continue;
+        uint32_t xw[64];
+        const u128 n2 = row_xbar(kp + i * HD, cs, xw, bad);
+        best = n2 > best ? n2 : best;
+    }
+    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const u128 o = shfl_xor_u128(best, m);
+        best = o > best ? o : best;
+    }
+    if (lane == 0) {
+        sm[warp][0] = (unsigned long long)best;
+        sm[warp][1] = (unsigned long long)(best >> 64);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        u128 m = 0;
+        for (int w = 0; w < 8; w++) {
+            u128 v = ((u128)sm[w][1] << 64) | (u128)sm[w][0];
+            m = v > m ? v : m;
+        }
+        st_q64(part_r2 + (unit * nsplit + split) * 2, (i128)m);
+    }
+}
+
+// Phase 3a, lane per key: grid (n_pad / 256, units), block 256 (thread = key i = 256 blockIdx.x + t).
+// Row r of tile i/128 in the UMMA canonical K-major layout: 16-B chunk kc of row r at
+// (kc*16 + r/8)*128 + (r%8)*16 -- 32 consecutive threads write 512 contiguous bytes per chunk.
+__global__ void __launch_bounds__(256) prep_x2_kernel(const uint16_t* __restrict__ k, int64_t n_local,
+                                                      int64_t n_pad, int mips, int KD,
+                                                      const float* __restrict__ center,
+                                                      const int64_t* __restrict__ r2, uint8_t* __restrict__ xt,
+                                                      float* __restrict__ xnorm, float* __restrict__ key_norm,
+                                                      uint32_t* status) {
+    __shared__ float cs[HD];
+    const int tid = threadIdx.x;
+    const int64_t unit = blockIdx.y;
+    if (tid < HD) cs[tid] = center[unit * HD + tid];
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * 256 + tid;
+    if (i >= n_pad) return;
+    const int r = (int)(i & 127);
+    uint8_t* tbase = xt + (unit * (n_pad >> 7) + (i >> 7)) * (int64_t)(128 * KD * 2) + (r >> 3) * 128 + (r & 7) * 16;
+    uint32_t xw[64];
+    bool bad = false;
+    u128 n2 = 0;
+    if (i < n_local) {
+        n2 = row_xbar(k + (unit * n_local + i) * HD, cs, xw, bad);
+    } else {
+#pragma unroll
+        for (int w = 0; w < 64; w++) xw[w] = 0u;
+    }
+    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
+#pragma unroll
+    for (int kc = 0; kc < 16; kc++)
+        *reinterpret_cast<uint4*>(tbase + kc * 16 * 128) =
+            make_uint4(xw[4 * kc], xw[4 * kc + 1], xw[4 * kc + 2], xw[4 * kc + 3]);
+    const double n2d = q64_to_double((i128)n2);
+    if (KD > HD) {
+        uint16_t sv = 0;
+        if (mips && i < n_local) {
+            const i128 diff = ld_q64(r2 + unit * 2) - (i128)n2;
+            sv = diff > 0 ? d2bf_rn_pos(sqrt(q64_to_double(diff))) : (uint16_t)0;
+        }
+        for (int kc = 16; kc < KD / 8; kc++)
+            *reinterpret_cast<uint4*>(tbase + kc * 16 * 128) = make_uint4(kc == 16 ? (uint32_t)sv : 0u, 0u, 0u, 0u);
+        const float sf = bf2f(sv);
+        const float nr = (float)sqrt(n2d + (double)sf * (double)sf);
+        xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
+        if (i < n_local) key_norm[unit * n_local + i] = nr;
+    } else {
+        const float nr = (float)sqrt(n2d);
+        xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
+        if (i < n_local) key_norm[unit * n_local + i] = nr;
     }
 }
 
@@ -213,7 +394,8 @@ __global__ void max_parts_kernel(const int64_t* __restrict__ part_r2, int nsplit
 // straight into the UMMA canonical K-major no-swizzle layout, one 128-row tile
 // per 128*KD*2 bytes: element (r, kk) at ((kk/8)*16 + r/8)*128 + (r%8)*16 + (kk%8)*2.
 // Also |xbar_i| (fp32, for the filter threshold; -1 for padding rows).
-// grid (ceil(n_pad/8), units), block 256 (warp per key)
+// grid (ceil(n_pad/(8*PX_KEYS)), units), block 256 (warp per PX_KEYS consecutive keys)
+constexpr int PX_KEYS = 8;
 __global__ void __launch_bounds__(256) prep_x_kernel(const uint16_t* __restrict__ k, int64_t n_local,
                                                      int64_t n_pad, int mips, int KD,
                                                      const float* __restrict__ center,
@@ -222,44 +404,54 @@ __global__ void __launch_bounds__(256) prep_x_kernel(const uint16_t* __restrict_
                                                      float* __restrict__ key_norm, uint32_t* status) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t unit = blockIdx.y;
-    const int64_t i = (int64_t)blockIdx.x * 8 + warp;
-    if (i >= n_pad) return;
-    const int64_t tile = i >> 7;
-    const int r = (int)(i & 127);
-    uint8_t* tbase = xt + (unit * (n_pad >> 7) + tile) * (int64_t)(128 * KD * 2);
-    const int rowoff = (r >> 3) * 128 + (r & 7) * 16;
-    uint32_t a = 0, b = 0;
-    u128 n2 = 0;
-    bool bad = false;
-    if (i < n_local) {
-        const float4 c = reinterpret_cast<const float4*>(center + unit * HD)[lane];
-        uint2 kr = reinterpret_cast<const uint2*>(k + (unit * n_local + i) * HD)[lane];
-        n2 = warp_sum_u128(transform4(kr, c, a, b, bad));
+    const int64_t ib = ((int64_t)blockIdx.x * 8 + warp) * PX_KEYS;  // this warp's PX_KEYS consecutive keys
+    if (ib >= n_pad) return;
+    const float4 c = reinterpret_cast<const float4*>(center + unit * HD)[lane];
+    uint2 kr[PX_KEYS];
+#pragma unroll
+    for (int u = 0; u < PX_KEYS; u++) {  // every row load in flight before the transforms
+        const int64_t i = ib + u;
+        kr[u] = i < n_local ? __ldg(reinterpret_cast<const uint2*>(k + (unit * n_local + i) * HD) + lane)
+                            : make_uint2(0u, 0u);
     }
-    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
-    // dims kk = 4*lane .. 4*lane+3: chunk kk/8 = lane/2, offset (lane&1)*8 bytes
-    *reinterpret_cast<uint2*>(tbase + (lane >> 1) * 16 * 128 + rowoff + (lane & 1) * 8) = make_uint2(a, b);
-    if (lane < (KD - HD) / 8) {
-        uint16_t s = 0;
-        double n2d = q64_to_double((i128)n2);
-        if (mips && lane == 0 && i < n_local) {
-            i128 rr = ld_q64(r2 + unit * 2);
-            i128 diff = rr - (i128)n2;
-            s = diff > 0 ? d2bf_rn_pos(sqrt(q64_to_double(diff))) : (uint16_t)0;
-        }
-        uint4 v = make_uint4((uint32_t)s, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(tbase + (16 + lane) * 16 * 128 + rowoff) = v;
-        if (lane == 0) {
-            float sf = bf2f(s);
-            float nr = (float)sqrt(n2d + (double)sf * (double)sf);
+    bool bad = false;
+    i128 rr = 0;
+    if (mips) rr = ld_q64(r2 + unit * 2);
+#pragma unroll
+    for (int u = 0; u < PX_KEYS; u++) {
+        const int64_t i = ib + u;
+        if (i >= n_pad) break;
+        const int64_t tile = i >> 7;
+        const int r = (int)(i & 127);
+        uint8_t* tbase = xt + (unit * (n_pad >> 7) + tile) * (int64_t)(128 * KD * 2);
+        const int rowoff = (r >> 3) * 128 + (r & 7) * 16;
+        uint32_t a = 0, b = 0;
+        u128 n2 = 0;
+        if (i < n_local) n2 = warp_sum_u128(transform4(kr[u], c, a, b, bad));
+        // dims kk = 4*lane .. 4*lane+3: chunk kk/8 = lane/2, offset (lane&1)*8 bytes
+        *reinterpret_cast<uint2*>(tbase + (lane >> 1) * 16 * 128 + rowoff + (lane & 1) * 8) = make_uint2(a, b);
+        if (lane < (KD - HD) / 8) {
+            uint16_t sv = 0;
+            double n2d = q64_to_double((i128)n2);
+            if (mips && lane == 0 && i < n_local) {
+                i128 diff = rr - (i128)n2;
+                sv = diff > 0 ? d2bf_rn_pos(sqrt(q64_to_double(diff))) : (uint16_t)0;
+            }
+            uint4 v = make_uint4((uint32_t)sv, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(tbase + (16 + lane) * 16 * 128 + rowoff) = v;
+            if (lane == 0) {
+                float sf = bf2f(sv);
+                float nr = (float)sqrt(n2d + (double)sf * (double)sf);
+                xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
+                if (i < n_local) key_norm[unit * n_local + i] = nr;
+            }
+        } else if (KD == HD && lane == 0) {
+            float nr = (float)sqrt(q64_to_double((i128)n2));
             xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
             if (i < n_local) key_norm[unit * n_local + i] = nr;
         }
-    } else if (KD == HD && lane == 0) {
-        float nr = (float)sqrt(q64_to_double((i128)n2));
-        xnorm[unit * n_pad + i] = i < n_local ? nr : -1.0f;
-        if (i < n_local) key_norm[unit * n_local + i] = nr;
     }
+    if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
 }
 
 // Phase 3b: projections W [dp][KL] fp32 -> bf16 tiles of 64 columns in the
@@ -326,8 +518,15 @@ int launch_key_norms(const uint16_t* k, int64_t units, int64_t n_local, int64_t 
     int nsplit = (int)((n_local + STATS_SPLIT - 1) / STATS_SPLIT);
     if (nsplit < 1) nsplit = 1;
     center_kernel<<<(unsigned)units, 128, 0, st>>>(key_sum, count, do_center, center);
-    r2_partial_kernel<<<dim3(nsplit, (unsigned)units), 256, 0, st>>>(k, n_local, seq_offset, n_global, sink,
-                                                                     local, center, part_r2, status);
+#ifndef MP_LANE_PER_KEY
+#define MP_LANE_PER_KEY 1
+#endif
+    if (MP_LANE_PER_KEY)
+        r2_partial2_kernel<<<dim3(nsplit, (unsigned)units), 256, 0, st>>>(k, n_local, seq_offset, n_global, sink,
+                                                                          local, center, part_r2, status);
+    else
+        r2_partial_kernel<<<dim3(nsplit, (unsigned)units), 256, 0, st>>>(k, n_local, seq_offset, n_global, sink,
+                                                                         local, center, part_r2, status);
     max_parts_kernel<<<(unsigned)((units + 127) / 128), 128, 0, st>>>(part_r2, nsplit, units, r2);
     count_launch(3);
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
@@ -346,8 +545,12 @@ int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad
                 const float* center, const int64_t* r2, uint8_t* xt, float* xnorm, float* key_norm, const float* W,
                 int KL, int NT, uint8_t* wt, float* wmax, uint32_t* status, cudaStream_t st) {
     cudaMemsetAsync(wmax, 0, sizeof(float), st);
-    prep_x_kernel<<<dim3((unsigned)((n_pad + 7) / 8), (unsigned)units), 256, 0, st>>>(
-        k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, key_norm, status);
+    if (MP_LANE_PER_KEY)
+        prep_x2_kernel<<<dim3((unsigned)((n_pad + 255) / 256), (unsigned)units), 256, 0, st>>>(
+            k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, key_norm, status);
+    else
+        prep_x_kernel<<<dim3((unsigned)((n_pad + 8 * PX_KEYS - 1) / (8 * PX_KEYS)), (unsigned)units), 256, 0, st>>>(
+            k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, key_norm, status);
     prep_w_kernel<<<NT, 64, 0, st>>>(W, HD + (mips ? 1 : 0), KL, KD, wt, wmax, status);
     count_launch(2);
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;

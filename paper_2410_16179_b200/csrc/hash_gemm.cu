@@ -23,7 +23,11 @@ namespace mp {
 constexpr int GM_R = 4;
 constexpr int GM_N = 64;
 constexpr int GM_STAGES = 3;
-constexpr int GM_THREADS = 64 + 256;  // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
+constexpr int GM_THREADS = 64 + 256;
+#ifndef MP_HG_RTU
+#define MP_HG_RTU 1
+#endif
+constexpr int HG_RTU = MP_HG_RTU;  // epilogue unroll over the 4 key tiles (code size vs the i-cache)  // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
 
 struct GemmParams {
     const uint8_t* xt;
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
             const int ts = c & 1;
             mbar_wait(t_full + ts, (c >> 1) & 1);
             tc_fence_after();
-#pragma unroll 1
+#pragma unroll HG_RTU
             for (int rt = 0; rt < GM_R; rt++) {
                 const int64_t kb = (m0 + rt * 128 + q * 32) >> 5;  // key block of this warp
                 const int64_t kchunk = kb >> 5;
@@ -148,17 +152,32 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                     const int j0 = c * GM_N + h * 32;
                     uint32_t w[32];
                     float mn = 3.0e38f;
+                    if (j0 + 32 <= p.KL && (j0 >> 2) + 8 <= p.KLq) {
+                        // interior columns (all but the last chunk): no per-column bounds
 #pragma unroll
-                    for (int cc = 0; cc < 32; cc++) {
-                        float a = __uint_as_float(v[cc]);
-                        w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
-                        if (j0 + cc < p.KL) mn = fminf(mn, fabsf(a));
-                    }
+                        for (int cc = 0; cc < 32; cc++) {
+                            const float a = __uint_as_float(v[cc]);
+                            w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
+                            mn = fminf(mn, fabsf(a));
+                        }
+                        uint4 sv = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-                    for (int qd = 0; qd < 8; qd++) {
-                        int jq = (j0 >> 2) + qd;
-                        if (lane == qd && jq < p.KLq)
-                            cw[(int64_t)jq * 32] = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+                        for (int qd = 0; qd < 8; qd++)
+                            if (lane == qd) sv = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+                        if (lane < 8) cw[(int64_t)((j0 >> 2) + lane) * 32] = sv;
+                    } else {
+#pragma unroll
+                        for (int cc = 0; cc < 32; cc++) {
+                            float a = __uint_as_float(v[cc]);
+                            w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
+                            if (j0 + cc < p.KL) mn = fminf(mn, fabsf(a));
+                        }
+#pragma unroll
+                        for (int qd = 0; qd < 8; qd++) {
+                            int jq = (j0 >> 2) + qd;
+                            if (lane == qd && jq < p.KLq)
+                                cw[(int64_t)jq * 32] = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+                        }
                     }
                     if (__any_sync(0xffffffffu, mn <= thr[rt])) {
                         const int64_t m = m0 + rt * 128 + q * 32 + lane;

@@ -607,32 +607,39 @@ __global__ void __launch_bounds__(NW * 32, 1) estimate_kernel(EstArgs a) {
 // CTA per (sequence, query head), thread per dimension: the log-sum-exp merge of the unit's warp records
 // in record order ("recursive attention"): M = max m_j, S = sum s_j e^{m_j - M},
 // A = sum a_j e^{m_j - M}, o = A / S.  PDL: waits for the estimator grid.
+// MS slices of HD threads: slice z merges records j = z, z + MS, ... (RB per load round), then slice 0
+// combines the MS partial states from shared memory in slice order (long contexts at small batch give a
+// unit hundreds of records: B=1 128K, 12 warps/SM -> 222 per unit)
+constexpr int MS = 4;
 template <int G>
-__global__ void __launch_bounds__(HD) merge_kernel(EstArgs a) {
+__global__ void __launch_bounds__(HD * MS) merge_kernel(EstArgs a) {
     constexpr int RB = 16;  // records per load round (all loads of a round in flight together)
     __shared__ int hsum[HD / 32];
+    __shared__ float pm[MS][HD], ps[MS][HD], pa[MS][HD];
     const int64_t row = blockIdx.x, b = row / a.Hq, hq = row % a.Hq;
     const int64_t g = hq % G, u = b * a.Hkv + hq / G;
-    const int d = threadIdx.x, lane = d & 31;
+    const int d = threadIdx.x % HD, z = threadIdx.x / HD, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    // |S_g| = sum over the unit's pieces (select step)
-    int hc = 0;
-    for (int64_t c = d; c < a.nchunks; c += HD) hc += __ldcg(a.hpc + row * a.nchunks + c);
+    if (z == 0) {  // |S_g| = sum over the unit's pieces (select step)
+        int hc = 0;
+        for (int64_t c = d; c < a.nchunks; c += HD) hc += __ldcg(a.hpc + row * a.nchunks + c);
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) hc += __shfl_xor_sync(0xffffffffu, hc, m);
-    if (lane == 0) hsum[d >> 5] = hc;
+        for (int m = 16; m >= 1; m >>= 1) hc += __shfl_xor_sync(0xffffffffu, hc, m);
+        if (lane == 0) hsum[d >> 5] = hc;
+    }
     const int2 rr = __ldcg(a.urec + u);
     const float* base = a.parts + ((size_t)(u + rr.x) * G + g) * PREC;
     const size_t stride = (size_t)G * PREC;
     const int np = rr.y;
     float M = -INFINITY, S = 0.0f, A = 0.0f;
 #pragma unroll 1
-    for (int j0 = 0; j0 < np; j0 += RB) {
+    for (int j0 = z; j0 < np; j0 += RB * MS) {
         float mj[RB], sj[RB], aj[RB];
 #pragma unroll
         for (int j = 0; j < RB; j++) {
-            const bool ok = j0 + j < np;
-            const float* rp = base + (size_t)(j0 + j) * stride;
+            const int jj = j0 + j * MS;
+            const bool ok = jj < np;
+            const float* rp = base + (size_t)jj * stride;
             mj[j] = ok ? __ldcg(rp) : -INFINITY;
             sj[j] = ok ? __ldcg(rp + 1) : 0.0f;
             aj[j] = ok ? __ldcg(rp + 4 + d) : 0.0f;
@@ -651,13 +658,26 @@ __global__ void __launch_bounds__(HD) merge_kernel(EstArgs a) {
         }
         M = Mn;
     }
+    pm[z][d] = M, ps[z][d] = S, pa[z][d] = A;
+    __syncthreads();
+    if (z != 0) return;
+    M = pm[0][d], S = ps[0][d], A = pa[0][d];
+#pragma unroll
+    for (int y = 1; y < MS; y++) {
+        const float My = pm[y][d];
+        const float Mn = fmaxf(M, My);
+        if (Mn == -INFINITY) continue;
+        const float f0 = M == -INFINITY ? 0.0f : __expf(M - Mn), f1 = My == -INFINITY ? 0.0f : __expf(My - Mn);
+        S = S * f0 + ps[y][d] * f1;
+        A = A * f0 + pa[y][d] * f1;
+        M = Mn;
+    }
     if (a.out) a.out[row * HD + d] = S > 0.0f ? A * (1.0f / S) : 0.0f;
     if (a.partial) {
         float* pp = a.partial + row * PART;
         pp[2 + d] = A;
         if (d == 0) pp[0] = M, pp[1] = S;
     }
-    __syncthreads();
     if (d == 0) {
         if (a.s_count) a.s_count[row] = hsum[0] + hsum[1] + hsum[2] + hsum[3];
         if (!(S > 0.0f) && a.out) atomicOr(a.status, MAGICPIG_STATUS_DEGENERATE);
@@ -730,7 +750,7 @@ template <int G>
 static int launch_merge_g(const EstArgs& a, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.B * a.Hq));
-    cfg.blockDim = dim3(HD);
+    cfg.blockDim = dim3(HD * v7::MS);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute attr;

@@ -89,6 +89,11 @@ __device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
 __device__ __forceinline__ void prefetch_l2_row(const void* p) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(p) : "memory");
 }
+// the same 256-B row by two plain L2 prefetches (LSU path, no TMA issue)
+__device__ __forceinline__ void prefetch_l2_row2(const uint16_t* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 64) : "memory");
+}
 // ln u(p) from the CTA's shared-memory copy of the table (see log_sampling_prob_lut)
 __device__ __forceinline__ float lnu_smem(const float* tab, float p, int K, int L, int minc) {
     if (p >= 1.0f) return 0.0f;
@@ -370,10 +375,25 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
         }
     };
 
+#ifndef MP_E9_PF
+#define MP_E9_PF 0
+#endif
+    // MP_E9_PF 2: the rows of the plan's slab into L2 by plain prefetches (lane r < 16: K row r, lane
+    // 16 + r: V row r), for the two slabs after the first at the start (a warp with few slabs would otherwise
+    // wait for each slab's rows in turn) and (3) also for slab s + 3 in every iteration
+    auto prefetch_plan = [&](const Plan& PL) {
+        const int r = lane & 15;
+        const int key = __shfl_sync(0xffffffffu, plan_key(PL), r);
+        if (r < PL.nr) prefetch_l2_row2((lane < 16 ? a.k : a.v) + ((int64_t)PL.u * a.n_local + key) * HD);
+    };
     Plan P0, P1, P2;
     plan_next(P0);
     plan_next(P1);
     plan_next(P2);
+    if (MP_E9_PF >= 2) {
+        prefetch_plan(P1);
+        prefetch_plan(P2);
+    }
     int cu = P0.u, cnr = P0.nr;
     issue_k(P0, xn0, xn1, bt0, bt1, key0, key1);
     issue_v(P0);
@@ -570,10 +590,7 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
         P0 = P1;
         P1 = P2;
         plan_next(P2);
-#ifndef MP_E9_PF
-#define MP_E9_PF 0
-#endif
-        if (MP_E9_PF) {   // rows of slab s + 3 into L2 (their registers are loaded two slabs later)
+        if (MP_E9_PF == 1) {   // rows of slab s + 3 into L2 (their registers are loaded two slabs later)
             const int r = lane & 15;
             const int key = __shfl_sync(0xffffffffu, plan_key(P1), r);
             if (r < P1.nr) {
@@ -581,6 +598,7 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
                 prefetch_l2_row((lane < 16 ? a.k : a.v) + row * HD);
             }
         }
+        if (MP_E9_PF >= 3) prefetch_plan(P1);
     }
     if (cur_u >= 0) flush(cur_u);
 }

@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(HD * MS) merge_kernel(EstArgs a) {
     const int64_t g = hq % G, u = b * a.Hkv + hq / G;
     const int d = threadIdx.x % HD, z = threadIdx.x / HD, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");  // the next step's encode (touches nothing read here)
     if (z == 0) {  // |S_g| = sum over the unit's pieces (select step)
         int hc = 0;
         for (int64_t c = d; c < a.nchunks; c += HD) hc += __ldcg(a.hpc + row * a.nchunks + c);

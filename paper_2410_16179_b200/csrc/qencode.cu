@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
         if (hb < BHq) qbits[hb * KLw + (j0 >> 5)] = wb;
     }
     __shared__ int lut_todo;
+    // the previous grid in the stream must be complete before this one is (see launch_qencode)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifndef MP_QE_LUTCHK
 #define MP_QE_LUTCHK 1
 #endif
@@ -165,12 +167,27 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
     }
 }
 
+#ifndef MP_QE_PDL
+#define MP_QE_PDL 0
+#endif
 int launch_qencode(const uint16_t* q, int64_t BHq, const float* W, int KL, int KLw, uint32_t* qbits,
                    uint32_t* status, cudaStream_t st, int K, int L, int minc, float* lutab) {
-    dim3 grid((unsigned)KLw, (unsigned)((BHq + QE_HEADS - 1) / QE_HEADS));
-    qencode_kernel<<<grid, QE_THREADS, 0, st>>>(q, BHq, W, KL, KLw, qbits, status, K, L, minc, lutab);
+    // PDL: the encode may start while the previous kernel in the stream (the previous decode's merge) runs;
+    // it touches nothing that kernel reads, and it waits for that grid before it completes, so everything
+    // after the encode stays ordered after the previous decode
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)KLw, (unsigned)((BHq + QE_HEADS - 1) / QE_HEADS));
+    cfg.blockDim = dim3(QE_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = MP_QE_PDL;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, qencode_kernel, q, BHq, W, KL, KLw, qbits, status, K, L, minc, lutab);
     count_launch(1);
-    return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
+    return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }
 
 }  // namespace mp

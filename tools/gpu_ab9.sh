@@ -9,7 +9,7 @@ for rep in 1 2; do
     MAGICPIG_LIB=$L timeout 600 python bench.py --kernel ${KV:-9} --steps 300 --sweep "${SWEEP:-}" --no-cpu-baseline --no-build --e2e-steps 20 ${BARGS:-} > $OUT/b.json 2>> $OUT/err.txt
     python -c "
 import json; d=json.load(open('$OUT/b.json'))
-print('$v', 'rep$rep', 'step', round(d['ms_per_step']*1e3,2), {k: round(v['us'],2) for k, v in d['kernels'].items()}, [(s['n'], s['B'], round(s['step_us'], 1), {k: round(v['us'], 1) for k, v in s['kernels'].items()}) for s in d.get('context_sweep', [])])" >> $OUT/ab.txt
+print('$v', 'rep$rep', 'step', round(d['ms_per_step']*1e3,2), {k: round(v['us'],2) for k, v in d['kernels'].items()}, [(s['n'], s['B'], round(s['step_us'], 1), {k: round(v['us'], 1) for k, v in s['kernels'].items()}) for s in (d.get('context_sweep') or [])])" >> $OUT/ab.txt
   done
 done
 cat $OUT/ab.txt

@@ -1,5 +1,5 @@
 """Small decodes for compute-sanitizer (memcheck / racecheck / synccheck): every decode kernel generation
-(5, 7, 8 and the automatic choice), dense codes and bucketed tables, an emulated 2-shard sequence split
+(5, 7, 8, 9 and the automatic choice), dense codes and bucketed tables, an emulated 2-shard sequence split
 (partial states + merge), at C1-like sizes.  Exits non-zero if an output is non-finite or a status is set.
   compute-sanitizer --tool memcheck python tools/sanitize_run.py"""
 from __future__ import annotations
@@ -28,7 +28,7 @@ def main():
         for buckets in (False, True):
             mp = pkg.MagicPIG(W, K=wl.K, L=wl.L, buckets=buckets).build(tk)
             ref = None
-            for kv in (0, 5, 7, 8):
+            for kv in (0, 5, 7, 8, 9):
                 B_.set_decode_kernel(kv)
                 out = mp.decode(tq, tk, tv)
                 torch.cuda.synchronize()

@@ -12,8 +12,9 @@
 // K*L columns streamed in N=64 chunks (3-stage bulk-copy ring).  Warp roles:
 //   warp 0: bulk-copy producer (cp.async.bulk + mbarrier complete_tx)
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-9: epilogue (tcgen05.ld 32x32b -> sign/filter -> ballot -> STG.128),
-//              two warps per TMEM lane quarter, 32 columns each
+//   warps 2..: epilogue (tcgen05.ld 32x32b -> sign/filter -> ballot -> STG.128),
+//              HG_EW / 4 warps per TMEM lane quarter, HG_CW columns each (16 warps x 16 columns
+//              by default: the epilogue, not the tensor pipe, paced the 8-warp version)
 // TMEM: 2 accumulator stages x (4 tiles x 64 columns) = 512 columns.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -23,11 +24,19 @@ namespace mp {
 constexpr int GM_R = 4;
 constexpr int GM_N = 64;
 constexpr int GM_STAGES = 3;
-constexpr int GM_THREADS = 64 + 256;
+#ifndef MP_HG_EW
+#define MP_HG_EW 16
+#endif
+constexpr int HG_EW = MP_HG_EW;              // epilogue warps: HG_EW / 4 per TMEM lane quarter
+constexpr int HG_CW = GM_N / (HG_EW / 4);    // columns of a chunk per epilogue warp (32 or 16)
+constexpr int GM_THREADS = 64 + 32 * HG_EW;  // producer, MMA, epilogue warps
 #ifndef MP_HG_RTU
 #define MP_HG_RTU 1
 #endif
 constexpr int HG_RTU = MP_HG_RTU;  // epilogue unroll over the 4 key tiles (code size vs the i-cache)  // producer, MMA, 8 epilogue warps (2 per TMEM lane quarter)
+
+__device__ __forceinline__ void tmem_ldn(uint32_t ta, uint32_t (&v)[32]) { tmem_ld32(ta, v); }
+__device__ __forceinline__ void tmem_ldn(uint32_t ta, uint32_t (&v)[16]) { tmem_ld16(ta, v); }
 
 struct GemmParams {
     const uint8_t* xt;
@@ -75,7 +84,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
         }
         for (int s = 0; s < 2; s++) {
             mbar_init(t_full + s, 1);
-            mbar_init(t_empty + s, 8);
+            mbar_init(t_empty + s, HG_EW);
         }
         fence_mbar_init();
     }
@@ -126,8 +135,9 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
     } else {
         // ---------------- epilogue ----------------
         const int q = warp & 3;            // TMEM lane quarter this warp may access
-        const int h = (warp - 2) >> 2;     // which 32 of the 64 columns of a chunk
+        const int h = (warp - 2) >> 2;     // which HG_CW of the 64 columns of a chunk
         const float wmax = *p.wmax;
+        const bool dbg = p.dbg_acc && blockIdx.x == 0 && blockIdx.y == 0;
         float thr[GM_R];
 #pragma unroll
         for (int rt = 0; rt < GM_R; rt++) {
@@ -146,44 +156,49 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                 const int lin = (int)(kb & 31);
                 uint4* cw = reinterpret_cast<uint4*>(p.codes) + ((unit * p.nchunks + kchunk) * p.KLq) * 32 + lin;
                 {
-                    uint32_t v[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ts * 256 + rt * GM_N + h * 32, v);
+                    uint32_t v[HG_CW];
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ts * 256 + rt * GM_N + h * HG_CW;
+                    tmem_ldn(ta, v);
                     tmem_wait_ld();
-                    const int j0 = c * GM_N + h * 32;
-                    uint32_t w[32];
+                    const int j0 = c * GM_N + h * HG_CW;
+                    uint32_t w[HG_CW];
                     float mn = 3.0e38f;
-                    if (j0 + 32 <= p.KL && (j0 >> 2) + 8 <= p.KLq) {
+                    constexpr int NQ = HG_CW / 4;  // uint4 stores (4 column words each)
+                    if (j0 + HG_CW <= p.KL && (j0 >> 2) + NQ <= p.KLq) {
                         // interior columns (all but the last chunk): no per-column bounds
 #pragma unroll
-                        for (int cc = 0; cc < 32; cc++) {
+                        for (int cc = 0; cc < HG_CW; cc++) {
                             const float a = __uint_as_float(v[cc]);
                             w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
                             mn = fminf(mn, fabsf(a));
                         }
-                        uint4 sv = make_uint4(0u, 0u, 0u, 0u);
+                        // the ballot words are warp-uniform: one lane stores them (no per-lane selects)
+                        if (lane == 0) {
 #pragma unroll
-                        for (int qd = 0; qd < 8; qd++)
-                            if (lane == qd) sv = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
-                        if (lane < 8) cw[(int64_t)((j0 >> 2) + lane) * 32] = sv;
+                            for (int qd = 0; qd < NQ; qd++)
+                                cw[(int64_t)((j0 >> 2) + qd) * 32] =
+                                    make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
+                        }
                     } else {
 #pragma unroll
-                        for (int cc = 0; cc < 32; cc++) {
+                        for (int cc = 0; cc < HG_CW; cc++) {
                             float a = __uint_as_float(v[cc]);
                             w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
                             if (j0 + cc < p.KL) mn = fminf(mn, fabsf(a));
                         }
 #pragma unroll
-                        for (int qd = 0; qd < 8; qd++) {
+                        for (int qd = 0; qd < NQ; qd++) {
                             int jq = (j0 >> 2) + qd;
                             if (lane == qd && jq < p.KLq)
                                 cw[(int64_t)jq * 32] = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
                         }
                     }
-                    if (__any_sync(0xffffffffu, mn <= thr[rt])) {
+                    const float th = rt == 0 ? thr[0] : (rt == 1 ? thr[1] : (rt == 2 ? thr[2] : thr[3]));
+                    if (__any_sync(0xffffffffu, mn <= th)) {
                         const int64_t m = m0 + rt * 128 + q * 32 + lane;
-                        for (int cc = 0; cc < 32; cc++) {
+                        for (int cc = 0; cc < HG_CW; cc++) {
                             float a = __uint_as_float(v[cc]);
-                            bool f = fabsf(a) <= thr[rt] && (j0 + cc) < p.KL;
+                            bool f = fabsf(a) <= th && (j0 + cc) < p.KL;
                             uint32_t fm = __ballot_sync(0xffffffffu, f);
                             if (fm) {
                                 uint32_t base = 0;
@@ -199,8 +214,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                             }
                         }
                     }
-                    if (p.dbg_acc && blockIdx.x == 0 && blockIdx.y == 0 && rt == 0) {
-                        for (int cc = 0; cc < 32; cc++)
+                    if (dbg && rt == 0) {
+                        for (int cc = 0; cc < HG_CW; cc++)
                             if (j0 + cc < p.KL) p.dbg_acc[(int64_t)(q * 32 + lane) * p.KL + j0 + cc] = __uint_as_float(v[cc]);
                     }
                 }

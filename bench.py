@@ -405,7 +405,7 @@ def measure_decode(rw, path, dev, tW, peaks, k, v, q, graph_steps=64, group=None
                 d(cfg, reps.qs[r], reps.tables(r) if path == "buckets" else reps.codes(r), reps.mps[r].buf.center,
                   reps.mps[r].buf.key_norm, reps.ks[r], reps.vs[r], 0, n, ws, out=out)
             us = _graph_time(dec, R, graph_steps)
-            names = {"decode": "decode5_kernel" + (" (+ bucket_mark_kernel)" if path == "buckets" else "")}
+            names = {"decode": "decode5_kernel" + (" (+ bucket_mark3_kernel)" if path == "buckets" else "")}
             ab["decode"] = ab["step"] - Bn * Hq * 256
             kern["decode"] = {"us": us, "alg_MB": ab["decode"] / 1e6}
         else:
@@ -416,7 +416,7 @@ def measure_decode(rw, path, dev, tW, peaks, k, v, q, graph_steps=64, group=None
             else:  # the select step is fused into the dense scan
                 ab["query"] += ab["select"]
             kern["estimate"] = {"us": _graph_time(stage(4), R, graph_steps), "note": "estimate + merge kernels"}
-            names = {"query": "bucket_mark_kernel" if path == "buckets" else "scan6_kernel (select fused)",
+            names = {"query": "bucket_mark3_kernel" if path == "buckets" else "scan6_kernel (select fused)",
                      "select": "select_kernel", "estimate": {7: "estimate_kernel", 8: "estimate8_kernel", 9: "estimate9_kernel"}[choice]}
             for nm in kern:
                 kern[nm]["alg_MB"] = ab[nm] / 1e6

@@ -133,22 +133,27 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
 
     for (int i = tid; i <= LUT_N; i += NW * 32) lut[i] = __ldg(a.lutab + i);
     {   // block exclusive scan of the piece lengths
-        // piece lengths: pcnt [units][nchunks] -> pref[u * P + 1 + c], eight loads in flight per thread
-        const int nch = (int)a.nchunks, NPc = (int)units * nch;
-        constexpr int NB = 8;
-        for (int i0 = tid; i0 < NPc; i0 += NW * 32 * NB) {
-            int v[NB];
+        // piece lengths: pcnt [units][nchunks] -> pref[u * P + 1 + c]; warp per unit, lane per chunk, four
+        // units (eight loads) in flight per lane, no integer division
+        const int nch = (int)a.nchunks;
+        for (int c0 = 0; c0 < nch; c0 += 64)
+            for (int u0 = warp; u0 < (int)units; u0 += NW * 4) {
+                int v[4][2];
 #pragma unroll
-            for (int j = 0; j < NB; j++) {
-                const int i = i0 + j * NW * 32;
-                v[j] = i < NPc ? __ldcg(a.pcnt + i) : 0;
-            }
+                for (int k = 0; k < 4; k++)
 #pragma unroll
-            for (int j = 0; j < NB; j++) {
-                const int i = i0 + j * NW * 32;
-                if (i < NPc) pref[i + i / nch + 1] = v[j];
+                    for (int h = 0; h < 2; h++) {
+                        const int u = u0 + k * NW, cc = c0 + lane + 32 * h;
+                        v[k][h] = (u < (int)units && cc < nch) ? __ldcg(a.pcnt + (int64_t)u * nch + cc) : 0;
+                    }
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int u = u0 + k * NW, cc = c0 + lane + 32 * h;
+                        if (u < (int)units && cc < nch) pref[u * P + 1 + cc] = v[k][h];
+                    }
             }
-        }
         for (int u = tid; u < (int)units; u += NW * 32) pref[u * P] = nT;
         __syncthreads();
         const int per = (NP + NW * 32 - 1) / (NW * 32);

@@ -334,8 +334,13 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
         sq += __shfl_xor_sync(0xffffffffu, sq, 1);
         sq += __shfl_xor_sync(0xffffffffu, sq, 2);
         const float qn = sqrtf(sq);
-        qn0 = __shfl_sync(0xffffffffu, qn, 4 * h0);
-        qn1 = __shfl_sync(0xffffffffu, qn, 4 * (h1 & 7));
+        if constexpr (G <= 4) {  // compact items: heads 2 (t4 & 1), 2 (t4 & 1) + 1
+            qn0 = __shfl_sync(0xffffffffu, qn, 4 * (2 * (t4 & 1)));
+            qn1 = __shfl_sync(0xffffffffu, qn, 4 * (2 * (t4 & 1) + 1));
+        } else {
+            qn0 = __shfl_sync(0xffffffffu, qn, 4 * h0);
+            qn1 = __shfl_sync(0xffffffffu, qn, 4 * (h1 & 7));
+        }
     };
     // leave unit u: record (m, s, a) of this warp -> parts[u + kw]; accumulator (dt, i) of rows g4 is
     // dimension 8 g4 + dt, of rows g4 + 8 dimension 64 + 8 g4 + dt
@@ -445,28 +450,59 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
         const int nu = P0.u, nnr = P0.nr;
         issue_k(P0, nxn0, nxn1, nbt0, nbt1, nk0, nk1);  // nr = 0: every load predicated off
 
-        // (2) items (row, head): ra = g4 (dl[0], dl[1]), rb = g4 + 8 (dl[2], dl[3]); heads h0, h1
-        const uint32_t bt[4] = {bt0, bt0, bt1, bt1};
-        const int hh[4] = {h0, h1, h0, h1};
-        bool need[4];
-        float cs[4];
-        {
-            const float qn[4] = {qn0, qn1, qn0, qn1};
-            const float xn[4] = {xn0, xn0, xn1, xn1};
+        // (2) items (row, head).  G = 8: every lane's four mma outputs, rows g4 (dl[0], dl[1]) and g4 + 8
+        // (dl[2], dl[3]), heads h0, h1.  G <= 4 (compact): columns 4..7 of the logits tile are empty, so lane
+        // t4 >= 2 takes over row g4 + 8 of lane t4 - 2 (xor 2) and every lane has two items, one row, heads
+        // 2 (t4 & 1) and 2 (t4 & 1) + 1; the per-head reductions then run over xor 2, 4, 8, 16.
+        constexpr bool CMP = G <= 4;
+        constexpr int NI = CMP ? 2 : 4;
+        const bool hirow = CMP && t4 >= 2;
+        float dlv[NI], dxv[NI];
+        uint32_t bt[NI];
+        int hh[NI], rows[NI];
+        float qnv[NI], xnv[NI];
+        if constexpr (CMP) {
+            const float sl2 = __shfl_xor_sync(0xffffffffu, dl[2], 2), sl3 = __shfl_xor_sync(0xffffffffu, dl[3], 2);
+            const float sx2 = __shfl_xor_sync(0xffffffffu, dx[2], 2), sx3 = __shfl_xor_sync(0xffffffffu, dx[3], 2);
+            dlv[0] = hirow ? sl2 : dl[0];
+            dlv[1] = hirow ? sl3 : dl[1];
+            dxv[0] = hirow ? sx2 : dx[0];
+            dxv[1] = hirow ? sx3 : dx[1];
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                bt[i] = hirow ? bt1 : bt0;
+                hh[i] = 2 * (t4 & 1) + i;
+                rows[i] = hirow ? g4 + 8 : g4;
+                xnv[i] = hirow ? xn1 : xn0;
+            }
+            qnv[0] = qn0, qnv[1] = qn1;
+        } else {
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                need[i] = hh[i] < G && !(bt[i] & 0x100u) && ((bt[i] >> hh[i]) & 1u);
-                const float den = qn[i] * xn[i];
-                const float c = den > 0.0f ? __fdividef(dx[i], den) : 0.0f;
-                cs[i] = fminf(1.0f, fmaxf(-1.0f, c));
+                dlv[i] = dl[i], dxv[i] = dx[i];
+                bt[i] = (i >> 1) ? bt1 : bt0;
+                hh[i] = (i & 1) ? h1 : h0;
+                rows[i] = (i >> 1) ? g4 + 8 : g4;
+                xnv[i] = (i >> 1) ? xn1 : xn0;
+                qnv[i] = (i & 1) ? qn1 : qn0;
             }
         }
-        float lu[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        bool need[NI];
+        float cs[NI];
+#pragma unroll
+        for (int i = 0; i < NI; i++) {
+            need[i] = hh[i] < G && !(bt[i] & 0x100u) && ((bt[i] >> hh[i]) & 1u);
+            const float den = qnv[i] * xnv[i];
+            const float c = den > 0.0f ? __fdividef(dxv[i], den) : 0.0f;
+            cs[i] = fminf(1.0f, fmaxf(-1.0f, c));
+        }
+        float lu[NI];
         {
-            int base = 0, pos[4];
+            int base = 0, pos[NI];
             const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
+            for (int i = 0; i < NI; i++) {
+                lu[i] = 0.0f;
                 const uint32_t bal = __ballot_sync(0xffffffffu, need[i]);
                 pos[i] = base + __popc(bal & lt);
                 base += __popc(bal);
@@ -475,7 +511,7 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
             __syncwarp();
             for (int e = lane; e < base; e += 32) {
                 const float p = 1.0f - acosf(wb.items[e]) * 0.3183098861837907f;
-                #ifndef MP_E9_SLUT
+#ifndef MP_E9_SLUT
 #define MP_E9_SLUT 1
 #endif
                 wb.items[e] = MP_E9_SLUT ? lnu_smem(lut, p, a.K, a.L, a.minc)
@@ -483,30 +519,32 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
             }
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < NI; i++)
                 if (need[i]) lu[i] = wb.items[pos[i]];
         }
-        float z[4];
+        float z[NI];
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const float l = dl[i] * INV_SQRT_D;
+        for (int i = 0; i < NI; i++) {
+            const float l = dlv[i] * INV_SQRT_D;
             z[i] = (hh[i] < G && (bt[i] & 0x100u)) ? l : (need[i] ? l - lu[i] : -INFINITY);
         }
         if (DBG) {
             const int64_t b = cur_u / a.Hkv, hkv = cur_u % a.Hkv, qh0 = b * a.Hq + hkv * G;
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int r = (i >> 1) ? g4 + 8 : g4;
-                if (z[i] != -INFINITY && r < cnr) {
-                    const int key = (i >> 1) ? key1 : key0;
+            for (int i = 0; i < NI; i++) {
+                if (z[i] != -INFINITY && rows[i] < cnr) {
+                    const int key = rows[i] >= 8 ? key1 : key0;
                     atomicOr(a.weighted + (qh0 + hh[i]) * nwb + (key >> 5), 1u << (key & 31));
                 }
             }
         }
-        // (3) online softmax per head (rows of head h are spread over the 8 lanes with the same t4)
-        float mx0 = fmaxf(z[0], z[2]), mx1 = fmaxf(z[1], z[3]);
+        // (3) online softmax per head (rows of head h are spread over the lanes with the same t4 (G = 8) or
+        // t4 & 1 (compact))
+        constexpr int MLO = CMP ? 2 : 4;
+        float mx0 = CMP ? z[0] : fmaxf(z[0], z[NI > 2 ? 2 : 0]);
+        float mx1 = CMP ? z[1] : fmaxf(z[1], z[NI > 2 ? 3 : 1]);
 #pragma unroll
-        for (int m = 4; m <= 16; m <<= 1) {
+        for (int m = MLO; m <= 16; m <<= 1) {
             mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, m));
             mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, m));
         }
@@ -514,12 +552,12 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
         const bool moved = __any_sync(0xffffffffu, mn0 != m0 || mn1 != m1);
         const float al0 = m0 == -INFINITY ? 0.0f : __expf(m0 - mn0);
         const float al1 = m1 == -INFINITY ? 0.0f : __expf(m1 - mn1);
-        const float mnn[4] = {mn0, mn1, mn0, mn1};
-        __nv_bfloat16 whi[4], wlo[4];
+        __nv_bfloat16 whi[NI], wlo[NI];
         float wsum0 = 0.0f, wsum1 = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const float w = z[i] == -INFINITY ? 0.0f : __expf(z[i] - mnn[i]);
+        for (int i = 0; i < NI; i++) {
+            const float mni = (i & 1) ? mn1 : mn0;
+            const float w = z[i] == -INFINITY ? 0.0f : __expf(z[i] - mni);
             whi[i] = __float2bfloat16_rn(w);
             wlo[i] = __float2bfloat16_rn(w - __bfloat162float(whi[i]));
             const float we = __bfloat162float(whi[i]) + __bfloat162float(wlo[i]);
@@ -527,7 +565,7 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
             else wsum0 += we;
         }
 #pragma unroll
-        for (int m = 4; m <= 16; m <<= 1) {
+        for (int m = MLO; m <= 16; m <<= 1) {
             wsum0 += __shfl_xor_sync(0xffffffffu, wsum0, m);
             wsum1 += __shfl_xor_sync(0xffffffffu, wsum1, m);
         }
@@ -537,9 +575,8 @@ __global__ void __launch_bounds__(nwarps<G>() * 32, 1) estimate9_kernel(EstArgs 
         m1 = mn1;
         {
             __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wb.wt);
-            const int rows[4] = {g4, g4, g4 + 8, g4 + 8};
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
+            for (int i = 0; i < NI; i++) {
                 if (hh[i] < G) {
                     wt[hh[i] * SR + rows[i]] = whi[i];
                     wt[(G + hh[i]) * SR + rows[i]] = wlo[i];

@@ -6,7 +6,9 @@
 //
 //   bucket_build_kernel  CTA per (unit, table): codes of the table from the bit
 //                        planes -> shared-memory histogram over 2^K buckets ->
-//                        exclusive scan -> offsets; scatter of key ids.
+//                        exclusive scan -> offsets; scatter of key ids (shared-memory atomics:
+//                        a bucket's ids are deterministic as a set, not in order; S is a
+//                        bitmap, so the Query result does not depend on the order).
 //   bucket_mark_kernel   CTA per (unit, query head): for each table the ids of
 //                        the query's bucket -> two shared-memory bitmaps
 //                        (seen >= 1, seen >= 2; a key is in exactly one bucket

@@ -454,16 +454,16 @@ __global__ void __launch_bounds__(256) prep_x_kernel(const uint16_t* __restrict_
     if (bad) atomicOr(status, MAGICPIG_STATUS_INEXACT);
 }
 
-// Phase 3b: projections W [dp][KL] fp32 -> bf16 tiles of 64 columns in the
-// same canonical layout (element (c, kk) at ((kk/8)*8 + c/8)*128 + (c%8)*16 +
-// (kk%8)*2), zero padded to KD rows and NT*64 columns; wmax = max_j |W_j|.
-// grid (NT), block 64 (thread = column)
-__global__ void __launch_bounds__(64) prep_w_kernel(const float* __restrict__ W, int dp, int KL, int KD,
+// Phase 3b: projections W [dp][KL] fp32 -> bf16 tiles of HG_N columns in the
+// same canonical layout (element (c, kk) at ((kk/8)*(HG_N/8) + c/8)*128 + (c%8)*16 +
+// (kk%8)*2), zero padded to KD rows and NT*HG_N columns; wmax = max_j |W_j|.
+// grid (NT), block HG_N (thread = column)
+__global__ void __launch_bounds__(HG_N) prep_w_kernel(const float* __restrict__ W, int dp, int KL, int KD,
                                                     uint8_t* __restrict__ wt, float* __restrict__ wmax,
                                                     uint32_t* status) {
     const int c = threadIdx.x;
-    const int j = blockIdx.x * 64 + c;
-    uint8_t* tbase = wt + (int64_t)blockIdx.x * (64 * KD * 2);
+    const int j = blockIdx.x * HG_N + c;
+    uint8_t* tbase = wt + (int64_t)blockIdx.x * (HG_N * KD * 2);
     const int rowoff = (c >> 3) * 128 + (c & 7) * 16;
     float nrm = 0.0f;
     bool notrepr = false;
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(64) prep_w_kernel(const float* __restrict__ W,
             }
             h[t] = lo | (hi << 16);
         }
-        *reinterpret_cast<uint4*>(tbase + kc * 8 * 128 + rowoff) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(tbase + kc * (HG_N / 8) * 128 + rowoff) = make_uint4(h[0], h[1], h[2], h[3]);
     }
     if (notrepr) atomicOr(status, MAGICPIG_STATUS_NOTREPR);
     // positive floats order like their bit patterns
@@ -551,7 +551,7 @@ int launch_prep(const uint16_t* k, int64_t units, int64_t n_local, int64_t n_pad
     else
         prep_x_kernel<<<dim3((unsigned)((n_pad + 8 * PX_KEYS - 1) / (8 * PX_KEYS)), (unsigned)units), 256, 0, st>>>(
             k, n_local, n_pad, mips, KD, center, r2, xt, xnorm, key_norm, status);
-    prep_w_kernel<<<NT, 64, 0, st>>>(W, HD + (mips ? 1 : 0), KL, KD, wt, wmax, status);
+    prep_w_kernel<<<NT, HG_N, 0, st>>>(W, HD + (mips ? 1 : 0), KL, KD, wt, wmax, status);
     count_launch(2);
     return cudaGetLastError() == cudaSuccess ? 0 : MAGICPIG_ECUDA;
 }

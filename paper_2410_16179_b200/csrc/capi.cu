@@ -92,8 +92,8 @@ static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, in
     if (w.nsplit < 1) w.nsplit = 1;
     w.KD = c->mips ? 144 : 128;
     int cols = g.KL > g.KLq * 4 ? g.KL : g.KLq * 4;
-    w.NT = (cols + 63) / 64;
-    int64_t dots = units * w.n_pad * (int64_t)w.NT * 64;
+    w.NT = (cols + HG_N - 1) / HG_N;
+    int64_t dots = units * w.n_pad * (int64_t)w.NT * HG_N;
     int64_t cap = dots / 512;
     if (cap < 65536) cap = 65536;
     if (cap > 0x7fffffffLL) cap = 0x7fffffffLL;
@@ -114,7 +114,7 @@ static BuildWs build_layout(const magicpig_config* c, int64_t B, int64_t Hkv, in
     w.part_r2 = (int64_t*)take((size_t)units * w.nsplit * 16);
     w.xt = take((size_t)units * w.n_pad * w.KD * 2);
     w.xnorm = (float*)take((size_t)units * w.n_pad * 4);
-    w.wt = take((size_t)w.NT * 64 * w.KD * 2);
+    w.wt = take((size_t)w.NT * HG_N * w.KD * 2);
     w.fix_list = (uint2*)take((size_t)w.fix_cap * 8);
     w.bytes = off;
     return w;

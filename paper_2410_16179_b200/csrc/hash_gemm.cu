@@ -8,28 +8,32 @@
 //   recomputed exactly in integers (fixup kernel), so every bit is the sign of
 //   the EXACT dot product (reading R6).
 //
-// CTA = 512 keys (4 M=128 tiles, A operand resident in shared memory) x all
-// K*L columns streamed in N=64 chunks (3-stage bulk-copy ring).  Warp roles:
+// CTA = GM_R M=128 key tiles (A operand resident in shared memory) x all K*L columns streamed in
+// N = GM_N chunks (bulk-copy ring).  Default GM_N = 128, GM_R = 2 (measured at C3: N = 64 x 4 tiles
+// 3908 us, N = 128 x 2 tiles 3266 us).  Warp roles:
 //   warp 0: bulk-copy producer (cp.async.bulk + mbarrier complete_tx)
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..: epilogue (tcgen05.ld 32x32b -> sign/filter -> ballot -> STG.128),
 //              HG_EW / 4 warps per TMEM lane quarter, HG_CW columns each (16 warps x 16 columns
 //              by default: the epilogue, not the tensor pipe, paced the 8-warp version)
-// TMEM: 2 accumulator stages x (4 tiles x 64 columns) = 512 columns.
+// TMEM: 2 accumulator stages x (GM_R tiles x GM_N columns) = 512 columns (4 x 64, or 2 x 128 with
+// MP_HG_N=128).
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace mp {
 
-constexpr int GM_R = 4;
-constexpr int GM_N = 64;
-constexpr int GM_STAGES = 3;
+constexpr int GM_R = HG_R;
+constexpr int GM_N = HG_N;
+constexpr int GM_STAGES = GM_N >= 256 ? 2 : 3;  // W chunk ring (shared memory: A tiles + stages <= 227 KB)
 #ifndef MP_HG_EW
 #define MP_HG_EW 16
 #endif
 constexpr int HG_EW = MP_HG_EW;              // epilogue warps: HG_EW / 4 per TMEM lane quarter
 constexpr int HG_CW = GM_N / (HG_EW / 4);    // columns of a chunk per epilogue warp (32 or 16)
 constexpr int GM_THREADS = 64 + 32 * HG_EW;  // producer, MMA, epilogue warps
+constexpr int HG_SUBW = HG_CW > 16 ? 16 : HG_CW;  // columns per TMEM load (bounds the registers)
+constexpr int HG_NSUB = HG_CW / HG_SUBW;
 #ifndef MP_HG_RTU
 #define MP_HG_RTU 1
 #endif
@@ -124,8 +128,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                 for (int rt = 0; rt < GM_R; rt++) {
                     for (int ks = 0; ks < KD / 16; ks++) {
                         uint64_t ad = umma_desc(a_base + rt * a_tile + ks * 2 * (16 * 128), 16 * 128, 128);
-                        uint64_t bd = umma_desc(b_base + s * b_tile + ks * 2 * (8 * 128), 8 * 128, 128);
-                        umma_bf16(tmem + ts * 256 + rt * GM_N, ad, bd, idesc, ks > 0 ? 1u : 0u);
+                        uint64_t bd = umma_desc(b_base + s * b_tile + ks * 2 * ((GM_N / 8) * 128), (GM_N / 8) * 128, 128);
+                        umma_bf16(tmem + ts * (GM_R * GM_N) + rt * GM_N, ad, bd, idesc, ks > 0 ? 1u : 0u);
                     }
                 }
                 umma_commit(b_empty + s);
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
     } else {
         // ---------------- epilogue ----------------
         const int q = warp & 3;            // TMEM lane quarter this warp may access
-        const int h = (warp - 2) >> 2;     // which HG_CW of the 64 columns of a chunk
+        const int h = (warp - 2) >> 2;     // which HG_CW of the GM_N columns of a chunk
         const float wmax = *p.wmax;
         const bool dbg = p.dbg_acc && blockIdx.x == 0 && blockIdx.y == 0;
         float thr[GM_R];
@@ -150,24 +154,26 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
             mbar_wait(t_full + ts, (c >> 1) & 1);
             tc_fence_after();
 #pragma unroll HG_RTU
-            for (int rt = 0; rt < GM_R; rt++) {
+            for (int rs = 0; rs < GM_R * HG_NSUB; rs++) {
+                const int rt = rs / HG_NSUB, sc = rs % HG_NSUB;  // key tile, 16-column piece of this warp's share
                 const int64_t kb = (m0 + rt * 128 + q * 32) >> 5;  // key block of this warp
                 const int64_t kchunk = kb >> 5;
                 const int lin = (int)(kb & 31);
                 uint4* cw = reinterpret_cast<uint4*>(p.codes) + ((unit * p.nchunks + kchunk) * p.KLq) * 32 + lin;
                 {
-                    uint32_t v[HG_CW];
-                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ts * 256 + rt * GM_N + h * HG_CW;
+                    uint32_t v[HG_SUBW];
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ts * (GM_R * GM_N) + rt * GM_N + h * HG_CW +
+                                        sc * HG_SUBW;
                     tmem_ldn(ta, v);
                     tmem_wait_ld();
-                    const int j0 = c * GM_N + h * HG_CW;
-                    uint32_t w[HG_CW];
+                    const int j0 = c * GM_N + h * HG_CW + sc * HG_SUBW;
+                    uint32_t w[HG_SUBW];
                     float mn = 3.0e38f;
-                    constexpr int NQ = HG_CW / 4;  // uint4 stores (4 column words each)
-                    if (j0 + HG_CW <= p.KL && (j0 >> 2) + NQ <= p.KLq) {
+                    constexpr int NQ = HG_SUBW / 4;  // uint4 stores (4 column words each)
+                    if (j0 + HG_SUBW <= p.KL && (j0 >> 2) + NQ <= p.KLq) {
                         // interior columns (all but the last chunk): no per-column bounds
 #pragma unroll
-                        for (int cc = 0; cc < HG_CW; cc++) {
+                        for (int cc = 0; cc < HG_SUBW; cc++) {
                             const float a = __uint_as_float(v[cc]);
                             w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
                             mn = fminf(mn, fabsf(a));
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                         }
                     } else {
 #pragma unroll
-                        for (int cc = 0; cc < HG_CW; cc++) {
+                        for (int cc = 0; cc < HG_SUBW; cc++) {
                             float a = __uint_as_float(v[cc]);
                             w[cc] = __ballot_sync(0xffffffffu, a > 0.0f);
                             if (j0 + cc < p.KL) mn = fminf(mn, fabsf(a));
@@ -193,10 +199,13 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                                 cw[(int64_t)jq * 32] = make_uint4(w[4 * qd], w[4 * qd + 1], w[4 * qd + 2], w[4 * qd + 3]);
                         }
                     }
-                    const float th = rt == 0 ? thr[0] : (rt == 1 ? thr[1] : (rt == 2 ? thr[2] : thr[3]));
+                    float th = thr[0];
+#pragma unroll
+                    for (int k = 1; k < GM_R; k++)
+                        if (rt == k) th = thr[k];
                     if (__any_sync(0xffffffffu, mn <= th)) {
                         const int64_t m = m0 + rt * 128 + q * 32 + lane;
-                        for (int cc = 0; cc < HG_CW; cc++) {
+                        for (int cc = 0; cc < HG_SUBW; cc++) {
                             float a = __uint_as_float(v[cc]);
                             bool f = fabsf(a) <= th && (j0 + cc) < p.KL;
                             uint32_t fm = __ballot_sync(0xffffffffu, f);
@@ -214,8 +223,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1) hash_gemm_kernel(GemmParams p) 
                             }
                         }
                     }
-                    if (dbg && rt == 0) {
-                        for (int cc = 0; cc < HG_CW; cc++)
+                    if (dbg && rt == 0) {  // (every piece sc of tile 0)
+                        for (int cc = 0; cc < HG_SUBW; cc++)
                             if (j0 + cc < p.KL) p.dbg_acc[(int64_t)(q * 32 + lane) * p.KL + j0 + cc] = __uint_as_float(v[cc]);
                     }
                 }
@@ -248,11 +257,11 @@ __global__ void __launch_bounds__(128) hash_fixup_kernel(const uint2* __restrict
         uint16_t xa[144], wa[144];
         const uint8_t* xb = xt + (unit * (n_pad >> 7) + (m >> 7)) * (int64_t)(128 * KD * 2);
         const int r = (int)(m & 127);
-        const uint8_t* wb = wt + (int64_t)(j >> 6) * (64 * KD * 2);
-        const int cidx = j & 63;
+        const uint8_t* wb = wt + (int64_t)(j / HG_N) * (HG_N * KD * 2);
+        const int cidx = j % HG_N;
         for (int kc = 0; kc < KD / 8; kc++) {
             uint4 xv = *reinterpret_cast<const uint4*>(xb + (kc * 16 + (r >> 3)) * 128 + (r & 7) * 16);
-            uint4 wv = *reinterpret_cast<const uint4*>(wb + (kc * 8 + (cidx >> 3)) * 128 + (cidx & 7) * 16);
+            uint4 wv = *reinterpret_cast<const uint4*>(wb + (kc * (HG_N / 8) + (cidx >> 3)) * 128 + (cidx & 7) * 16);
             const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, ws[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
             for (int t = 0; t < 4; t++) {

@@ -5,7 +5,12 @@
 
 namespace mp {
 
-constexpr int STATS_SPLIT = 1024;  // keys per partial-statistics CTA
+constexpr int STATS_SPLIT = 1024;
+#ifndef MP_HG_N
+#define MP_HG_N 128
+#endif
+constexpr int HG_N = MP_HG_N;              // hash GEMM: columns per W tile / MMA N (64, 128 or 256)
+constexpr int HG_R = 256 / HG_N;           // hash GEMM: 128-key tiles per CTA (TMEM: 2 stages x HG_R x HG_N = 512)  // keys per partial-statistics CTA
 constexpr int DEC_THREADS = 256;   // decode CTA (8 warps)
 
 void count_launch(int n);

@@ -31,6 +31,30 @@ __device__ __forceinline__ void qe_mma(float (&d)[4], const uint32_t (&a)[4], ui
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// rare: the dot recomputed in fp64 (certified at 2^-44), then exactly; out of line so that the hot path of
+// the encode stays small in the instruction cache
+__device__ __noinline__ int qe_slow_sign(const uint16_t* __restrict__ qh, const uint16_t* wcol, uint32_t* status) {
+    double sd = 0.0, bd = 0.0;
+    for (int d = 0; d < HD; d++) {
+        const double pq = (double)bf2f(qh[d]) * (double)bf2f(wcol[d]);
+        sd += pq;
+        bd += fabs(pq);
+    }
+    if (fabs(sd) > 0x1p-44 * bd) return sd > 0.0;
+    uint16_t xa[HD], wv[HD];
+    for (int d = 0; d < HD; d++) {
+        xa[d] = qh[d];
+        wv[d] = wcol[d];
+    }
+    return exact_dot_sign_bf16(xa, wv, HD, status) > 0;
+}
+// the ln u table (once per (K, L, min_collisions)), out of line for the same reason
+__device__ __noinline__ void qe_fill_lut(float* lutab, int K, int L, int minc) {
+    const int nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+    for (int i = bid * QE_THREADS + threadIdx.x; i <= LUT_N; i += nb * QE_THREADS)
+        lutab[i] = (float)log_sampling_prob_d((double)LUT_P0 + (double)i * (1.0 - (double)LUT_P0) / LUT_N, K, L, minc);
+}
+
 __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __restrict__ q, int64_t BHq,
                                                              const float* __restrict__ W, int KL, int KLw,
                                                              uint32_t* __restrict__ qbits, uint32_t* status,
@@ -104,23 +128,7 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
 #define MP_QE_CERT 0x1p-16f
 #endif
             if (live && !(fabsf(s) > MP_QE_CERT * bnd[nt][e])) {
-                // rare: this thread recomputes the dot in fp64, then exactly
-                double sd = 0.0, bd = 0.0;
-                for (int d = 0; d < HD; d++) {
-                    const double pq = (double)bf2f(q[h * HD + d]) * (double)bf2f(wsm[col][d]);
-                    sd += pq;
-                    bd += fabs(pq);
-                }
-                if (fabs(sd) > 0x1p-44 * bd) {
-                    bit = sd > 0.0;
-                } else {
-                    uint16_t xa[HD], wv[HD];
-                    for (int d = 0; d < HD; d++) {
-                        xa[d] = q[h * HD + d];
-                        wv[d] = wsm[col][d];
-                    }
-                    bit = exact_dot_sign_bf16(xa, wv, HD, status) > 0;
-                }
+                bit = qe_slow_sign(q + h * HD, wsm[col], status);
             }
             if (bit && live) {
                 if (e >> 1) wb |= 1u << col;
@@ -150,10 +158,8 @@ __global__ void __launch_bounds__(QE_THREADS) qencode_kernel(const uint16_t* __r
         if (threadIdx.x == 0) lut_todo = __ldcg(hdr) != want;
         __syncthreads();
         if (lut_todo) {
-            const int nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
-            for (int i = bid * QE_THREADS + threadIdx.x; i <= LUT_N; i += nb * QE_THREADS)
-                lutab[i] = (float)log_sampling_prob_d((double)LUT_P0 + (double)i * (1.0 - (double)LUT_P0) / LUT_N,
-                                                      K, L, minc);
+            const int nb = gridDim.x * gridDim.y;
+            qe_fill_lut(lutab, K, L, minc);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();

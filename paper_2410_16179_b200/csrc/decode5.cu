@@ -20,7 +20,7 @@
 //                   by bulk copies (3-deep), logits q.k/sqrt(d) and the
 //                   hashed-vector dots on tensor cores (mma.sync bf16), p, log u
 //                   (R5, R11), z = logit - log u, an online
-//                   softmax whose a[g][d] accumulates on tensor cores (tf32).
+//                   softmax whose a[g][d] accumulates on tensor cores (tf32 hi + lo weights).
 //                   When the unit changes they flush the unit's partial state
 //                   (m, s, |S|, a) and the last CTA of a unit merges its partials
 //                   in fixed order (log-sum-exp, "recursive attention" P:171).
@@ -713,9 +713,9 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                 const float mo = f.mrun[g];
                 const float mn = fmaxf(mo, mb);
                 const float sc = (mo == -INFINITY) ? 0.0f : __expf(mo - mn);
-                // weights rounded to tf32 (the accumulation MMA's input); the normaliser sums the same
-                // rounded weights, so the estimate stays a convex combination of the value rows
-                const float w = (z == -INFINITY) ? 0.0f : to_tf32(__expf(z - mn));
+                // fp32 weights; the P.V MMA takes them as tf32 hi + lo parts (two MMAs, ~2^-21 relative
+                // per weight), so heavy cancellation in the value rows (|o| << |v|) stays accurate
+                const float w = (z == -INFINITY) ? 0.0f : __expf(z - mn);
                 const float wsum = warp_sum_f(w);
                 f.w[rr][g] = w;
                 __syncwarp();  // every lane has read f.mrun[g] before lane 0 replaces it
@@ -739,8 +739,10 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
 #pragma unroll
                 for (int ks = 0; ks < RB / 8; ks++) {
                     const int k0 = ks * 8 + (lane & 3), k1 = k0 + 4;
-                    const uint32_t a0 = g < G ? __float_as_uint(f.w[k0][g]) : 0u;
-                    const uint32_t a2 = g < G ? __float_as_uint(f.w[k1][g]) : 0u;
+                    const float w0 = g < G ? f.w[k0][g] : 0.0f, w1 = g < G ? f.w[k1][g] : 0.0f;
+                    const float h0 = to_tf32(w0), h1 = to_tf32(w1);
+                    const uint32_t a0 = __float_as_uint(h0), a2 = __float_as_uint(h1);
+                    const uint32_t l0 = __float_as_uint(to_tf32(w0 - h0)), l2 = __float_as_uint(to_tf32(w1 - h1));
 #pragma unroll
                     for (int nt = 0; nt < 4; nt++) {
                         const int dcol = gw * 32 + nt * 8 + (lane >> 2);
@@ -749,6 +751,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
                         const uint32_t v1 =
                             k1 < nb ? (uint32_t)*reinterpret_cast<const uint16_t*>(buf + k1 * ROWB + 256 + dcol * 2) << 16 : 0u;
                         mma1688_tf32(acc[nt], a0, a2, v0, v1);
+                        mma1688_tf32(acc[nt], l0, l2, v0, v1);
                     }
                 }
             }

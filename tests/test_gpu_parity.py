@@ -421,3 +421,30 @@ def test_weighted_set_is_s_union_t(G, buckets, decode_kernel):
                 np.testing.assert_array_equal(s_bits, (ref["in_s"][g] == 1).astype(np.uint8))
                 np.testing.assert_array_equal(w_bits, (ref["in_s"][g] >= 1).astype(np.uint8))
                 assert _rel_err(out.cpu().numpy()[b, row], ref["out"][g]) <= TOL
+
+
+@pytest.mark.gpu
+def test_value_cancellation():
+    """Heavy cancellation in P.V (|o| << |v|): keys come in pairs (row 2j+1 = row 2j with dimension 0 moved by
+    one bf16 ulp, so the pair's weights differ by ~1e-4 relative and its hash codes almost always agree) whose
+    values are +64 and -64 (plus small noise).  The R18 tolerance relative to max|o| then needs the weights at
+    about fp32 accuracy inside the P.V products (kernel 5: tf32 hi + lo parts; kernels 7-9: bf16 hi + lo);
+    weights rounded once to tf32 would lose the pairs' difference."""
+    wl = synth.Workload("cancel", 777, B=1, Hq=4, Hkv=1, n=3000, K=10, L=150)
+    k, v, q = synth.make_batch(wl)
+    k = k.copy()
+    k[:, :, 1::2] = k[:, :, 0::2]
+    k[:, :, 1::2, 0] = np.where(k[:, :, 1::2, 0] == 0xFFFF, 0xFFFE, k[:, :, 1::2, 0] + 1).astype(np.uint16)
+    rng = np.random.default_rng(4242)
+    sgn = np.where(np.arange(wl.n) % 2 == 0, 1.0, -1.0).reshape(1, 1, wl.n, 1)
+    vf = 64.0 * sgn + 0.25 * rng.standard_normal((1, 1, wl.n, 128))
+    v = synth.bf16_bits_from_f32(vf)
+    W = synth.make_projections(wl.K, wl.L, wl.mips)
+    res = _run_gpu(wl, k, v, q, W)
+    assert res["status_build"] == 0 and res["status_decode"] == 0
+    ref = oracle.decode_batch(k, v, q, W, wl.K, wl.L, wl.center, wl.mips, wl.min_collisions, wl.sink, wl.local)[0][0]
+    vmax = float(np.max(np.abs(synth.bf16_bits_to_f32(v))))
+    for g in range(wl.G):
+        assert np.max(np.abs(ref["out"][g])) < vmax / 16, "the case must cancel"
+        err = _rel_err(res["out"][0, g], ref["out"][g])
+        assert err <= TOL, (g, err)

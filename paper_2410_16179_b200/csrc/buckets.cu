@@ -296,8 +296,14 @@ __global__ void __launch_bounds__(BM2_THREADS) bucket_mark2_kernel(const uint32_
 // seen-twice bitmaps; after a cluster barrier CTA 0 combines them through distributed shared memory with the
 // same saturating counter, (a1, a2) + (b1, b2) = (a1 | b1, a2 | b2 | (a1 & b1)), and writes S.  Splitting a
 // head over two SMs halves the heaviest head's time (the C3 heads' id counts are skewed: max ~1.9x the mean).
-constexpr int BM3_THREADS = 512;
-constexpr int BM3_UNROLL = 4;
+#ifndef MP_BM3_THREADS
+#define MP_BM3_THREADS 512
+#endif
+#ifndef MP_BM3_UNROLL
+#define MP_BM3_UNROLL 4
+#endif
+constexpr int BM3_THREADS = MP_BM3_THREADS;
+constexpr int BM3_UNROLL = MP_BM3_UNROLL;
 #ifndef MP_BM3_CS
 #define MP_BM3_CS 2
 #endif

@@ -468,7 +468,7 @@ static int decode_impl(const magicpig_config* cfg, const uint16_t* q, int64_t Hq
         if (rc) return rc;
         a.sbits = w.sbits;
     }
-    const int64_t tiles = B * Hkv * (g.nchunks * (v5 ? decode5_halves(a, num_sms()) : 1) + a.nstatic);
+    const int64_t tiles = B * Hkv * (g.nchunks + a.nstatic);  // one tile per 1024-key chunk
     const int64_t grid = v5 ? (tiles < num_sms() ? tiles : num_sms()) : tiles * a.tsplit;
     if (grid_out) *grid_out = grid;
     if (timeline) {

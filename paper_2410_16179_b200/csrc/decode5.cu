@@ -777,12 +777,6 @@ __global__ void __launch_bounds__(THREADS, 1) decode5_kernel(DecodeArgs a) {
 // ---- host: shared-memory layout and launch
 static size_t al128(size_t x) { return (x + 127) & ~(size_t)127; }
 
-// chunk tiles per 1024-key chunk: 1 (512-key half tiles were measured slower and removed)
-int decode5_halves(const DecodeArgs& a, int nsm) {
-    (void)a;
-    (void)nsm;
-    return 1;
-}
 
 // fills the v5 layout fields of a; returns the dynamic smem bytes, or 0 if v5 does not fit
 size_t decode5_layout(DecodeArgs& a, int G, int max_smem) {

@@ -83,7 +83,6 @@ constexpr int BM_PARTS = MP_BM_PARTS;  // id slices per (sequence, query head) i
 int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, int64_t Hq, int64_t Hkv,
                        int64_t n_local, int K, int L, int KLw, int minc, uint32_t* sbits, cudaStream_t st,
                        int parts = 1);
-int decode5_halves(const DecodeArgs& a, int nsm);
 int launch_merge(const float* parts, int P, int64_t BH, float* out, cudaStream_t st);
 int launch_empty_partial(float* partial, int64_t BH, cudaStream_t st);
 

@@ -91,13 +91,30 @@ def main():
                 tk, tv, tq = t(k[None, None]), t(v[None, None]), t(q[None])
                 mp = pkg.MagicPIG(torch.from_numpy(W).to(dev), K=K, L=L).build(tk)
                 got = mp.decode(tq, tk, tv).cpu().numpy()[0]
+            # readings R3 / R5 in the paper's literal forms, oracle only:
+            # R3 literal: c and the MIPS radius r over all n keys (sink + local included), same T
+            idx_all = oracle.build_unit(k, W, K, L, base.center, base.mips, sink=0, local=0)
+            idx_all.update(sink=base.sink, local=base.local)
+            r3 = oracle.decode_indexed(idx_all, k, v, q, base.min_collisions)
             for g in range(base.G):
                 qf = bf(q[g]).astype(np.float64)
                 w = oracle.softmax_f64(kf @ qf / np.sqrt(128.0))
                 exact = oracle.expectation(w, vf)
+                sel = ref["in_s"][g]
+                # the estimator re-run on Alg. 1's own S and ln u reproduces the decode (harness self-check)
+                assert rel(oracle.estimate(q[g], k, v, sel, ref["logu"][g])["out"], ref["out"][g]) < 1e-12
+                # R5 literal: p_i from the raw cos(q, k_i) = w_i / (|q| |k_i|) instead of the hashed
+                # vectors qbar, xbar_i; same S, only the weights ln u_i change
+                cosr = np.clip(kf @ qf / np.maximum(np.linalg.norm(kf, axis=1) * np.linalg.norm(qf), 1e-300), -1, 1)
+                lu5 = np.zeros(len(sel))
+                for i in np.nonzero(sel == 1)[0]:
+                    lu5[i] = np.log(oracle.sampling_prob(1.0 - np.arccos(cosr[i]) / np.pi, K, L, base.min_collisions))
+                est5 = oracle.estimate(q[g], k, v, sel, lu5)["out"]
                 row = next(r for r in results["rows"] if r["unit"] == h and r["head"] == g and r["values"] == wname)
                 cost = int(np.count_nonzero(ref["in_s"][g]))
-                ent = {"K": K, "L": L, "cost": cost, "sampled": int(ref["s_count"][g]), "err_oracle": rel(ref["out"][g], exact)}
+                ent = {"K": K, "L": L, "cost": cost, "sampled": int(ref["s_count"][g]), "err_oracle": rel(ref["out"][g], exact),
+                       "err_R5_literal": rel(est5, exact), "err_R3_literal": rel(r3["out"][g], exact),
+                       "cost_R3_literal": int(np.count_nonzero(r3["in_s"][g]))}
                 if got is not None:
                     ent["err_gpu"] = rel(got[g].astype(np.float64), exact)
                     ent["gpu_vs_oracle"] = rel(got[g].astype(np.float64), ref["out"][g])
@@ -115,7 +132,10 @@ def main():
         for i, (K, L) in enumerate(KL):
             pts = [r["magicpig"][i] for r in rows]
             e = {"cost": float(np.mean([p["cost"] for p in pts])),
-                 "err_oracle": float(np.mean([p["err_oracle"] for p in pts]))}
+                 "err_oracle": float(np.mean([p["err_oracle"] for p in pts])),
+                 "err_R5_literal": float(np.mean([p["err_R5_literal"] for p in pts])),
+                 "err_R3_literal": float(np.mean([p["err_R3_literal"] for p in pts])),
+                 "cost_R3_literal": float(np.mean([p["cost_R3_literal"] for p in pts]))}
             if "err_gpu" in pts[0]:
                 e["err_gpu"] = float(np.mean([p["err_gpu"] for p in pts]))
                 e["gpu_vs_oracle_max"] = float(np.max([p["gpu_vs_oracle"] for p in pts]))
@@ -123,7 +143,10 @@ def main():
         summ[wname] = sw
     results["summary"] = summ
     results["note"] = ("err = ||estimate - exact|| / ||exact||, exact = fp64 softmax attention over all n keys; cost = "
-                       "tokens whose K/V rows are read; MagicPIG cost includes the static set T (sink + local)")
+                       "tokens whose K/V rows are read; MagicPIG cost includes the static set T (sink + local); "
+                       "err_R5_literal: the same S weighted with p from the raw cos(q, k) (P:111) instead of the hashed "
+                       "vectors (reading R5); err_R3_literal / cost_R3_literal: c and r over all n keys (P:127) instead "
+                       "of D (reading R3), oracle only")
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(results, f, indent=1)

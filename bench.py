@@ -249,7 +249,7 @@ def make_rank_inputs(rw, threads):
 
 
 # ----------------------------------------------------------------------------- algorithmic bytes
-def alg_bytes(cfg_wl, B, Hq, Hkv, n, n_union, nT, path, ids_read=0):
+def alg_bytes(cfg_wl, B, Hq, Hkv, n, n_union, nT, path, ids_read=0, id_bytes=4):
     """Per step: query (codes of D, or bucket ids + offsets; + S bitmaps written), select (S bitmaps read,
     lists written), estimator (K/V rows + |xbar| of union_g S_g u T, lists read, q, c)."""
     KL = cfg_wl.K * cfg_wl.L
@@ -258,7 +258,7 @@ def alg_bytes(cfg_wl, B, Hq, Hkv, n, n_union, nT, path, ids_read=0):
     if path == "dense":
         q_read = B * Hkv * nD * KL / 8 + B * Hq * KL / 8
     else:
-        q_read = ids_read * 4 + B * Hq * cfg_wl.L * 8 + B * Hq * KL / 8
+        q_read = ids_read * id_bytes + B * Hq * cfg_wl.L * 8 + B * Hq * KL / 8
     query = q_read + sbits
     select = sbits + n_union * 4 + B * Hkv * 4 + B * Hq * 4
     rows = (n_union + B * Hkv * nT)
@@ -363,7 +363,7 @@ def measure_decode(rw, path, dev, tW, peaks, k, v, q, graph_steps=64, group=None
         B_.query_codes(cfg, reps.qs[0], tW, qc, ws)
         qc = qc.cpu().numpy().view(np.uint16).astype(np.int64)
         nb = 1 << wl.K
-        per = wl.L * (nb + 1 + n)
+        per = B_.bucket_tables_words(cfg, 1, 1, n)  # words per unit (16-bit ids when n <= 65536)
         tabs = reps.mps[0].buf.tables
         for b in range(Bn):
             for hq in range(Hq):
@@ -371,7 +371,7 @@ def measure_decode(rw, path, dev, tW, peaks, k, v, q, graph_steps=64, group=None
                 offs = tabs[u * per:u * per + wl.L * (nb + 1)].view(wl.L, nb + 1).cpu().numpy()
                 c = qc[b, hq]
                 ids_read += int((offs[np.arange(wl.L), c + 1] - offs[np.arange(wl.L), c]).sum())
-    ab = alg_bytes(wl, Bn, Hq, Hkv, n, n_union, nT, path, ids_read)
+    ab = alg_bytes(wl, Bn, Hq, Hkv, n, n_union, nT, path, ids_read, 2 if n <= 65536 else 4)
 
     if partial:
         def step(r):

@@ -189,10 +189,13 @@ int magicpig_decode_encoded(const magicpig_config* cfg, const uint16_t* q, int64
  * sampled sets S_g are identical to the dense scan's (a key lies in exactly one
  * bucket per table, so "in the query's bucket of >= min_collisions tables" is
  * the P:84 rule).  Requires K <= 14 and ceil(n_local/32)*8 <= 200 KiB.
- * Layout, int32 words: tables[B*Hkv][ L*(2^K+1) offsets | L*n_local ids ]:
+ * Layout, int32 words: tables[B*Hkv][ L*(2^K+1) int32 offsets | L*n_local ids ]:
  *   offsets[t][c] .. offsets[t][c+1]  = the range of ids[t][] with code c
  *   ids[t][e]                         = local key index (ascending within a
- *                                       bucket is NOT guaranteed)
+ *                                       bucket is NOT guaranteed); uint16 when
+ *                                       n_local <= 65536 (the paper's int16
+ *                                       entries; the id part is then
+ *                                       ceil(L*n_local/2) words), else int32
  * magicpig_bucket_tables_words: size of `tables` (0 if unsupported). [host]
  * magicpig_build_buckets: builds them from the packed codes of
  *   magicpig_build_tables (call after it, same shapes).

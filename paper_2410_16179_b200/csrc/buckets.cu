@@ -28,6 +28,18 @@ namespace cgr = cooperative_groups;
 constexpr int BK_THREADS = 512;
 constexpr int BM_THREADS = 512;
 
+// key ids are stored as 16-bit words when every local index fits (n_local <= 65536: the paper's int16
+// table entries), else as int32.  Per unit: L*(2^K+1) int32 offsets, then the L*n_local ids.
+__host__ __device__ __forceinline__ bool ids16(int64_t n_local) { return n_local <= 65536; }
+__host__ __device__ __forceinline__ size_t unit_words(int L, int nb, int64_t n_local) {
+    const size_t ne = (size_t)L * (size_t)n_local;
+    return (size_t)L * ((size_t)nb + 1) + (ids16(n_local) ? (ne + 1) / 2 : ne);
+}
+// id number idx of a unit's id array (ids0 = the unit's first id word)
+__device__ __forceinline__ int load_id(const int32_t* __restrict__ ids0, size_t idx, bool narrow) {
+    return narrow ? (int)__ldg(reinterpret_cast<const unsigned short*>(ids0) + idx) : __ldg(ids0 + idx);
+}
+
 // code of table t for the 32 keys of block blk (bit r of word b = column t*K+b of key 32*blk+r)
 __device__ __forceinline__ void table_words(const uint32_t* __restrict__ cu, int KLq, int K, int t, int64_t blk,
                                             uint32_t (&w)[16]) {
@@ -95,9 +107,11 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_build_kernel(const uint32_t
     const int64_t u = blockIdx.y;
     const int nb = 1 << K;
     const uint32_t* cu = codes + (size_t)u * nchunks * KLq * 128;
-    int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    int32_t* tu = tables + (size_t)u * unit_words(L, nb, n_local);
     int32_t* offs = tu + (size_t)t * (nb + 1);
-    int32_t* ids = tu + (size_t)L * (nb + 1) + (size_t)t * n_local;
+    const bool narrow = ids16(n_local);
+    int32_t* ids = tu + (size_t)L * (nb + 1) + (narrow ? 0 : (size_t)t * n_local);
+    uint16_t* ids_h = reinterpret_cast<uint16_t*>(tu + (size_t)L * (nb + 1)) + (size_t)t * n_local;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     const int64_t nblk = (n_local + 31) >> 5;
@@ -118,7 +132,8 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_build_kernel(const uint32_t
         const int nr = (int)min((int64_t)32, n_local - blk * 32);
         for (int r = 0; r < nr; r++) {
             const int pos = atomicAdd(&hist[key_code(w, K, r)], 1);
-            ids[pos] = (int32_t)(blk * 32 + r);
+            if (narrow) ids_h[pos] = (uint16_t)(blk * 32 + r);
+            else ids[pos] = (int32_t)(blk * 32 + r);
         }
     }
 }
@@ -150,7 +165,8 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
     int* lo_s = reinterpret_cast<int*>(seen + 2 * nw);
     int* start = lo_s + L;
     const int tid = threadIdx.x;
-    const int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    const int32_t* tu = tables + (size_t)u * unit_words(L, nb, n_local);
+    const bool narrow = ids16(n_local);
     for (int64_t w = tid; w < 2 * nw; w += blockDim.x) seen[w] = 0u;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
     const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(BM_THREADS) bucket_mark_kernel(const uint32_t*
             ids[j] = -1;
             if (e < e_end) {
                 while (e >= tnext) tnext = start[++t + 1];
-                ids[j] = __ldg(ids0 + (size_t)t * n_local + lo_s[t] + (e - start[t]));
+                ids[j] = load_id(ids0, (size_t)t * n_local + lo_s[t] + (e - start[t]), narrow);
             }
         }
 #pragma unroll
@@ -233,7 +249,8 @@ __global__ void __launch_bounds__(BM2_THREADS) bucket_mark2_kernel(const uint32_
     int* len_s = lo_s + L;
     int* cstart = len_s + L;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    const int32_t* tu = tables + (size_t)u * unit_words(L, nb, n_local);
+    const bool narrow = ids16(n_local);
     for (int w = tid; w < 2 * nw; w += BM2_THREADS) seen[w] = 0u;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
     const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
@@ -270,7 +287,7 @@ __global__ void __launch_bounds__(BM2_THREADS) bucket_mark2_kernel(const uint32_
             if (c < C) {
                 while (c >= cstart[t + 1]) t++;
                 const int off = ((c - cstart[t]) << 5) + lane;
-                if (off < len_s[t]) ids[j] = __ldg(ids0 + (size_t)t * n_local + lo_s[t] + off);
+                if (off < len_s[t]) ids[j] = load_id(ids0, (size_t)t * n_local + lo_s[t] + off, narrow);
             }
         }
 #pragma unroll
@@ -308,6 +325,7 @@ constexpr int BM3_UNROLL = MP_BM3_UNROLL;
 #define MP_BM3_CS 2
 #endif
 constexpr int BM3_CS = MP_BM3_CS;
+template <bool NARROW>  // NARROW: 16-bit ids (n_local <= 65536), a compile-time load width
 __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_t* __restrict__ qbits,
                                                                     const int32_t* __restrict__ tables, int64_t Hq,
                                                                     int64_t Hkv, int64_t n_local, int K, int L,
@@ -330,7 +348,8 @@ __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_
     int* len_s = base_s + L;
     int* cstart = len_s + L;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int32_t* tu = tables + (size_t)u * L * ((size_t)nb + 1 + n_local);
+    const int32_t* tu = tables + (size_t)u * unit_words(L, nb, n_local);
+    constexpr bool narrow = NARROW;
     for (int w = tid; w < 2 * nw; w += BM3_THREADS) seen[w] = 0u;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
     const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
@@ -373,7 +392,7 @@ __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_
             if (c < cw1) {
                 while (c >= cstart[t + 1]) t++;
                 const int off = ((c - cstart[t]) << 5) + lane;
-                if (off < len_s[t]) ids[j] = __ldg(ids0 + base_s[t] + off);
+                if (off < len_s[t]) ids[j] = load_id(ids0, (size_t)base_s[t] + off, narrow);
             }
         }
 #pragma unroll
@@ -406,7 +425,7 @@ __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_
 }
 
 size_t bucket_tables_words(int K, int L, int64_t units, int64_t n_local) {
-    return (size_t)units * L * (((size_t)1 << K) + 1 + (size_t)n_local);
+    return (size_t)units * unit_words(L, 1 << K, n_local);
 }
 
 int launch_bucket_build(const uint32_t* codes, int64_t units, int64_t n_local, int K, int L, int KLq,
@@ -431,9 +450,9 @@ int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, 
     if (MP_BM2 == 3 && parts == 1 && (int64_t)L * n_local < (1ll << 31)) {
         const size_t smem3 = (size_t)((n_local + 31) >> 5) * 8 + (size_t)(3 * L + 1) * 4;
         if (smem3 <= 208 * 1024) {
-            if (smem3 > 48 * 1024 && cudaFuncSetAttribute(bucket_mark3_kernel,
-                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          (int)smem3) != cudaSuccess)
+            auto kern = ids16(n_local) ? bucket_mark3_kernel<true> : bucket_mark3_kernel<false>;
+            if (smem3 > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3) != cudaSuccess)
                 return MAGICPIG_ECUDA;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)(Hq * BM3_CS), (unsigned)B, 1u);
@@ -449,7 +468,7 @@ int launch_bucket_mark(const uint32_t* qbits, const int32_t* tables, int64_t B, 
             attr[1].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 2;
-            cudaError_t e = cudaLaunchKernelEx(&cfg, bucket_mark3_kernel, qbits, tables, Hq, Hkv, n_local, K, L, KLw,
+            cudaError_t e = cudaLaunchKernelEx(&cfg, kern, qbits, tables, Hq, Hkv, n_local, K, L, KLw,
                                                minc, sbits);
             count_launch(1);
             return e == cudaSuccess ? 0 : MAGICPIG_ECUDA;

@@ -50,6 +50,8 @@ CASES = [
     ("tiny", 37, 1, 1, 1, 2, 3, 1, 1, 2, 1, 1),
     ("manyunits", 3000, 16, 32, 8, 8, 20, 1, 1, 2, 4, 64),
     ("longg8", 20000, 1, 8, 1, 6, 16, 1, 1, 2, 4, 64),
+    ("ids16max", 65536, 1, 2, 1, 7, 10, 1, 1, 2, 4, 64),  # largest n with uint16 ids (id 65535)
+    ("ids32", 70001, 1, 2, 1, 6, 12, 1, 1, 2, 4, 64),     # n > 65536: int32 ids
 ]
 
 
@@ -100,14 +102,15 @@ def test_bucket_contents_are_the_code_classes():
     mp, _ = _build(wl, k, W)
     tables = mp.buf.tables.cpu().numpy()
     nb = 1 << wl.K
-    per_unit = wl.L * (nb + 1 + wl.n)
+    # n <= 65536: the ids are uint16 (the paper's int16 table entries), ceil(L*n/2) words
+    per_unit = wl.L * (nb + 1) + (wl.L * wl.n + 1) // 2
     assert tables.size == pkg.binding.bucket_tables_words(mp.cfg, 1, 2, wl.n) == 2 * per_unit
     for h in range(2):
         t_ = oracle.key_transform(k[0, h], wl.sink, wl.local, 1, 1)
         codes = oracle.encode_keys(t_["xbar"], W, wl.K, wl.L)  # [n][L]
         tu = tables[h * per_unit:(h + 1) * per_unit]
         offs = tu[:wl.L * (nb + 1)].reshape(wl.L, nb + 1)
-        ids = tu[wl.L * (nb + 1):].reshape(wl.L, wl.n)
+        ids = np.ascontiguousarray(tu[wl.L * (nb + 1):]).view(np.uint16)[:wl.L * wl.n].reshape(wl.L, wl.n)
         for t in range(wl.L):
             assert offs[t, 0] == 0 and offs[t, nb] == wl.n and np.all(np.diff(offs[t]) >= 0)
             for c in np.unique(codes[:, t]):

@@ -91,7 +91,7 @@ def run(name, R=4, G_STEPS=64, buckets=0, **over):
         B_.query_codes(cfg, tq, tW, qc, ws)
         qc = qc.cpu().numpy().view(np.uint16).astype(np.int64)
         nb = 1 << wl.K
-        per = wl.L * (nb + 1 + n)
+        per = B_.bucket_tables_words(cfg, 1, 1, n)  # words per unit (16-bit ids when n <= 65536)
         tabs = mps[0].buf.tables.cpu().numpy()
         ids_read = 0
         for b in range(Bn):
@@ -100,7 +100,7 @@ def run(name, R=4, G_STEPS=64, buckets=0, **over):
                 offs = tabs[u * per:u * per + wl.L * (nb + 1)].reshape(wl.L, nb + 1)
                 c = qc[b, hq]
                 ids_read += int((offs[np.arange(wl.L), c + 1] - offs[np.arange(wl.L), c]).sum())
-        alg = alg - Bn * Hkv * (n - nT) * KL / 8 + ids_read * 4 + Bn * Hq * wl.L * 8 + 2 * Bn * Hq * ((n + 31) // 32) * 4
+        alg = alg - Bn * Hkv * (n - nT) * KL / 8 + ids_read * (2 if n <= 65536 else 4) + Bn * Hq * wl.L * 8 + 2 * Bn * Hq * ((n + 31) // 32) * 4
         res["ids_read"] = ids_read
     res.update(config=name, n=n, B=Bn, K=wl.K, L=wl.L, alg_MB=alg / 1e6, buckets=buckets,
                sampled=float(scount.float().mean()) / max(n - nT, 1), union=n_union,

@@ -74,6 +74,18 @@ def test_codes_words_layout(K, L):
             assert want * 4 >= B * Hkv * n * K * L / 8
 
 
+@pytest.mark.parametrize("K,L", [(10, 150), (7, 35), (14, 6), (3, 5)])
+def test_bucket_tables_words_layout(K, L):
+    """bucket_tables_words = units * (L*(2^K+1) int32 offsets + ids): the L*n ids take 16 bits each when
+    n <= 65536 (the paper's int16 table entries; ceil(L*n/2) words), 32 bits above (header layout)."""
+    from paper_2410_16179_b200 import binding
+    cfg = binding.make_config(K=K, L=L)
+    for B, Hkv, n in [(1, 1, 1), (1, 8, 16384), (2, 3, 1025), (1, 1, 65536), (1, 2, 65537), (1, 1, 100001)]:
+        ids = -(-(L * n) // 2) if n <= 65536 else L * n
+        assert binding.bucket_tables_words(cfg, B, Hkv, n) == B * Hkv * (L * ((1 << K) + 1) + ids)
+    assert binding.bucket_tables_words(binding.make_config(K=15, L=L), 1, 1, 1000) == 0  # K <= 14 only
+
+
 def test_workspace_sizes_positive():
     from paper_2410_16179_b200 import binding
     cfg = binding.make_config()

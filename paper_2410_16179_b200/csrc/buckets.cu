@@ -350,6 +350,11 @@ __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t* tu = tables + (size_t)u * unit_words(L, nb, n_local);
     constexpr bool narrow = NARROW;
+#ifndef MP_BM3_PAIR
+#define MP_BM3_PAIR 0
+#endif
+    // 16-bit ids two per lane per load: parity-green but measured slower at C3 (Query 16.97 vs 15.77 us), off
+    constexpr bool PAIR = NARROW && MP_BM3_PAIR;
     for (int w = tid; w < 2 * nw; w += BM3_THREADS) seen[w] = 0u;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // query codes of the encode kernel
     const uint32_t* qb = qbits + (b * Hq + hq) * KLw;
@@ -362,7 +367,8 @@ __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_
         const int lo = __ldg(offs + qc), hi = __ldg(offs + qc + 1);
         base_s[t] = (int)((int64_t)t * n_local + lo);  // < L * n_local (checked on the host)
         len_s[t] = hi - lo;
-        cstart[t] = (hi - lo + 31) >> 5;
+        // PAIR: 64-id chunks of aligned 32-bit id pairs (the range widened to an even start)
+        cstart[t] = PAIR ? (hi > lo ? (hi - lo + (base_s[t] & 1) + 63) >> 6 : 0) : (hi - lo + 31) >> 5;
     }
     __syncthreads();
     const int C = block_exclusive_scan(cstart, L, warp_tot);  // cstart[t] = first chunk of table t
@@ -384,24 +390,40 @@ __global__ void __launch_bounds__(BM3_THREADS) bucket_mark3_kernel(const uint32_
         t = lo;
     }
     for (int c0 = cw0; c0 < cw1; c0 += BM3_UNROLL) {
-        int ids[BM3_UNROLL];
+        int ids[BM3_UNROLL][PAIR ? 2 : 1];
 #pragma unroll
         for (int j = 0; j < BM3_UNROLL; j++) {
             const int c = c0 + j;
-            ids[j] = -1;
+#pragma unroll
+            for (int h = 0; h < (PAIR ? 2 : 1); h++) ids[j][h] = -1;
             if (c < cw1) {
                 while (c >= cstart[t + 1]) t++;
-                const int off = ((c - cstart[t]) << 5) + lane;
-                if (off < len_s[t]) ids[j] = load_id(ids0, (size_t)base_s[t] + off, narrow);
+                if constexpr (PAIR) {
+                    // id elements e, e + 1 of the unit's array in one aligned 32-bit load (little endian)
+                    const int b = base_s[t], end = b + len_s[t];
+                    const int e = (b & ~1) + ((c - cstart[t]) << 6) + 2 * lane;
+                    if (e + 1 >= b && e < end) {
+                        const uint32_t w =
+                            __ldg(reinterpret_cast<const unsigned int*>(reinterpret_cast<const uint16_t*>(ids0) + e));
+                        if (e >= b) ids[j][0] = (int)(w & 0xffffu);
+                        if (e + 1 < end) ids[j][1] = (int)(w >> 16);
+                    }
+                } else {
+                    const int off = ((c - cstart[t]) << 5) + lane;
+                    if (off < len_s[t]) ids[j][0] = load_id(ids0, (size_t)base_s[t] + off, narrow);
+                }
             }
         }
 #pragma unroll
         for (int j = 0; j < BM3_UNROLL; j++) {
-            if (ids[j] >= 0) {
-                const int i = ids[j];
-                const uint32_t bit = 1u << (i & 31);
-                const uint32_t old = atomicOr(&seen1[i >> 5], bit);
-                if (minc > 1 && (old & bit)) atomicOr(&seen2[i >> 5], bit);
+#pragma unroll
+            for (int h = 0; h < (PAIR ? 2 : 1); h++) {
+                if (ids[j][h] >= 0) {
+                    const int i = ids[j][h];
+                    const uint32_t bit = 1u << (i & 31);
+                    const uint32_t old = atomicOr(&seen1[i >> 5], bit);
+                    if (minc > 1 && (old & bit)) atomicOr(&seen2[i >> 5], bit);
+                }
             }
         }
     }
